@@ -1,0 +1,427 @@
+"""NanoSpec draft-head benchmark (BASELINE.json metric: us per draft LM-head step
+and achieved HBM GB/s at Llama-3.1-8B shape vs the dense head).
+
+    python bench.py [--gpus N --steps K --warmup W] [--config llama|qwen|tiny]
+                    [--n-nodes 60 --k 10 --head auto|simt|tc] [--impl ours|reference]
+
+A step is one pass of the hot path for one sequence: the state
+update a2 (60 draft-tree tokens + 3 verify tokens appended, window slid, I
+recompacted) followed by the head a3+a4+a5 (gathered contraction over I and
+per-node top-k with global ids).  Inputs are synthetic and resident in HBM;
+the active set is exactly W_max = 3072 rows (the headline), and
+successive steps rotate over R sequences with pairwise-disjoint id pools so
+every step reads rows that are not in L2 (R x 25.2 MB > 126 MB L2).
+
+Multi-GPU (torchrun): data-parallel, each rank runs its own sequences (weak
+scaling, no collective on the path); value = max-over-ranks device time /
+(steps x ranks).  `--impl reference` times the CPU oracle instead (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "µs per draft LM-head step and achieved HBM GB/s at Llama-3.1-8B shape vs dense head"
+
+CONFIGS = {
+    "llama": dict(model="llama-3.1-8b", vocab=128256, d=4096, w_max=3072),
+    "qwen": dict(model="qwen-2.5-7b", vocab=152064, d=3584, w_max=3072),
+    "tiny": dict(model="tiny", vocab=1000, d=64, w_max=256),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="llama", choices=list(CONFIGS))
+    ap.add_argument("--n-nodes", type=int, default=60)
+    ap.add_argument("--k", type=int, default=10)
+    ap.add_argument("--head", default="auto", choices=["auto", "simt", "tc"])
+    ap.add_argument("--rotate", type=int, default=24, help="sequences with disjoint id pools (cold L2)")
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-sample-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the GPU is under load."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- reference arm (CPU oracle)
+def cpu_oracle_steps(cfg, n_nodes, k, steps, seed=0):
+    """Runs `steps` full oracle steps (state update by Eq. 4/5 over the retained
+    window + fp64 restricted head + top-k + lse) on the host; returns us/step and
+    a description.  The oracle is used as it stands (single-threaded C)."""
+    import torch
+
+    from oracle import oracle as O
+    from synthetic import inputs as SI
+    V, d, Wm = cfg["vocab"], cfg["d"], cfg["w_max"]
+    pools = SI.disjoint_pools(V, Wm + 128, 1, seed=3)
+    prompt, ups = SI.cyclic_fresh_updates(pools[0], Wm, steps)
+    Wt = SI.bf16_weights(V, d, seed=0)
+    Wb = SI.bf16_bits(Wt)
+    H = SI.bf16_bits(SI.bf16_hidden(n_nodes, d, seed=1))
+    ref = O.OracleStream(V, Wm).init(prompt)
+    t0 = time.perf_counter()
+    for dr, vr in ups:
+        ref.update(dr, vr)
+        ref.S = ref.S[-Wm:]  # only the window matters for Eq. 5; keeps the host stream bounded
+        ids, _ = ref.active()
+        z, _ = O.logits(Wb, H, ids, want_abs=False)
+        O.topk(z, ids, k)
+        O.lse(z)
+    dt = time.perf_counter() - t0
+    return dt / steps * 1e6, f"{steps} full steps (|I|={len(ids)}, n={n_nodes}, k={k}) of the {cfg['model']} workload"
+
+
+def run_reference(args):
+    """The reference arm: the CPU oracle, as it stands, on the same workload.
+    If K+W full steps would take more than ~2 minutes, every step computes a
+    bounded sample of the draft nodes and the time is scaled to all nodes
+    (the head's cost is linear in n; the state update is always done in full)."""
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    n = args.n_nodes
+    t_one, _ = cpu_oracle_steps(cfg, n, args.k, 1)
+    budget_us = 120e6
+    steps = max(1, args.steps)
+    n_s = n
+    if (steps + args.warmup) * t_one > budget_us:
+        n_s = max(1, int(n * budget_us / ((steps + args.warmup) * t_one)))
+    if args.warmup:
+        cpu_oracle_steps(cfg, n_s, args.k, min(args.warmup, 3))
+    us, sample = cpu_oracle_steps(cfg, n_s, args.k, steps)
+    us = us * n / n_s
+    if n_s != n:
+        sample += f"; {n_s} of {n} nodes per step, time scaled x{n / n_s:.2f}"
+    line = {
+        "metric": METRIC, "value": round(us, 1), "unit": "us/step", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": us / 1e3, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"{cfg['model']} draft head: V={cfg['vocab']} d={cfg['d']} |I|={cfg['w_max']} "
+                               f"n={n} k={args.k} batch=1"},
+        "cpu_baseline": {"value": round(us, 1), "unit": "us/step", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": round(us, 1), "unit": "us/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_26444_b200 as P
+    from synthetic import inputs as SI
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS[args.config]
+    V, d, Wm = cfg["vocab"], cfg["d"], cfg["w_max"]
+    n, k = args.n_nodes, args.k
+    n_upd = 60 + 3
+    R = args.rotate
+    pool = Wm + 2 * n_upd
+    R = max(1, min(R, V // pool))
+    W = SI.bf16_weights(V, d, seed=0, device=dev)
+    pools = SI.disjoint_pools(V, pool, R, seed=3 + rank)
+    total_steps_per_seq = (args.warmup + 2 * args.steps + 2 * R) // R + 4
+    states, outs, upd_d, upd_v = [], [], [], []
+    Hs = SI.bf16_hidden(n, d, seed=1 + rank, device=dev, batch=R)
+    for r in range(R):
+        prompt, ups = SI.cyclic_fresh_updates(pools[r], Wm, total_steps_per_seq)
+        st = P.ActiveVocab(V, Wm, device=dev)
+        st.init(0, torch.as_tensor(prompt, device=dev))
+        states.append(st)
+        outs.append(P.HeadOutputs(1, n, k, Wm, dev))
+        upd_d.append(torch.as_tensor(np.stack([u[0] for u in ups]), device=dev))
+        upd_v.append(torch.as_tensor(np.stack([u[1] for u in ups]), device=dev))
+    cursor = [0] * R
+
+    def step(s):
+        r = s % R
+        c = cursor[r]
+        cursor[r] += 1
+        states[r].update(0, upd_d[r][c], upd_v[r][c])
+        P.draft_logits_topk(states[r], W, Hs[r:r + 1], k, impl=args.head, out=outs[r])
+
+    def head_only(s):
+        r = s % R
+        P.draft_logits_topk(states[r], W, Hs[r:r + 1], k, impl=args.head, out=outs[r])
+
+    stream = torch.cuda.current_stream(dev)
+    # warm-up (eager: also sets function attributes), then one captured warm-up graph
+    for s in range(args.warmup):
+        step(s)
+    torch.cuda.synchronize()
+    assert all(st.read(0)["n_active"] == Wm for st in states), "headline |I| must be exactly W_max"
+
+    def capture(fn, count, start):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for s in range(start, start + count):
+                fn(s)
+        return g
+
+    K = args.steps
+    g_steps = capture(step, K, args.warmup)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        g_steps.replay()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        ms_total = ev0.elapsed_time(ev1)
+        # head-only graph (idempotent) replayed for a longer soak: per-call head time + clock samples
+        g_head = capture(head_only, K, 0)
+        head_ms = []
+        t_end = time.time() + 1.0
+        while time.time() < t_end or len(head_ms) < 3:
+            ev0.record(stream)
+            g_head.replay()
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            head_ms.append(ev0.elapsed_time(ev1) / K)
+    torch.cuda.synchronize()
+    if world > 1:
+        t = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    assert all(st.read(0)["n_active"] == Wm for st in states)
+    us_step = ms_total * 1e3 / K
+    us_head = statistics.median(head_ms) * 1e3
+
+    # state update alone (its own graph over the next fresh updates)
+    def upd_only(s):
+        r = s % R
+        c = cursor[r]
+        cursor[r] += 1
+        states[r].update(0, upd_d[r][c], upd_v[r][c])
+
+    U = 2 * R
+    g_upd = capture(upd_only, U, 0)
+    ev0.record(stream)
+    g_upd.replay()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    us_upd = ev0.elapsed_time(ev1) * 1e3 / U
+
+    # e2e through the public API with host buffers: H2D hidden + update ids, D2H top-k + lse
+    Hh = Hs[0].cpu().pin_memory()
+    ud_h = [upd_d[r].cpu().pin_memory() for r in range(R)]
+    uv_h = [upd_v[r].cpu().pin_memory() for r in range(R)]
+    out_l = torch.empty(n, k, dtype=torch.float32).pin_memory()
+    out_i = torch.empty(n, k, dtype=torch.int32).pin_memory()
+    out_s = torch.empty(n, dtype=torch.float32).pin_memory()
+    Hd = torch.empty(1, n, d, dtype=torch.bfloat16, device=dev)
+    ud_d = torch.empty(60, dtype=torch.int32, device=dev)
+    uv_d = torch.empty(3, dtype=torch.int32, device=dev)
+    E = K
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for s in range(E):
+        r = s % R
+        c = cursor[r]
+        cursor[r] += 1
+        Hd.copy_(Hh, non_blocking=True)
+        ud_d.copy_(ud_h[r][c], non_blocking=True)
+        uv_d.copy_(uv_h[r][c], non_blocking=True)
+        states[r].update(0, ud_d, uv_d)
+        tl, ti, ts, _ = P.draft_logits_topk(states[r], W, Hd, k, impl=args.head, out=outs[r])
+        out_l.copy_(tl[0], non_blocking=True)
+        out_i.copy_(ti[0], non_blocking=True)
+        out_s.copy_(ts[0], non_blocking=True)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    us_e2e = ev0.elapsed_time(ev1) * 1e3 / E
+    assert all(st.read(0)["n_active"] == Wm for st in states)
+    h2d = Hh.numel() * 2 + 63 * 4
+    d2h = n * k * 8 + n * 4
+
+    # dense comparators: cuBLAS bf16 GEMM (fp32 accumulate) + torch.topk, and our head over [0, V)
+    dense = {}
+    if not args.no_dense:
+        Hd1 = Hs[0]
+        mm_f32 = _mm_out_dtype_ok(torch)
+
+        def cublas():
+            zz = torch.mm(Hd1, W.t(), out_dtype=torch.float32) if mm_f32 else torch.mm(Hd1, W.t()).float()
+            return torch.topk(zz, k, dim=1)
+
+        for _ in range(3):
+            cublas()
+        torch.cuda.synchronize()
+        reps = 20
+        ev0.record(stream)
+        for _ in range(reps):
+            cublas()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        dense["cublas_topk_us"] = ev0.elapsed_time(ev1) * 1e3 / reps
+        dense["cublas_fp32_out"] = bool(mm_f32)
+        allids = torch.arange(V, dtype=torch.int32, device=dev)
+        nid = torch.tensor([V], dtype=torch.int32, device=dev)
+        o_dense = P.HeadOutputs(1, n, k, V, dev)
+        for _ in range(3):
+            P.logits_topk_ids(allids, nid, W, Hd1, k, impl=args.head, out=o_dense)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(reps):
+            P.logits_topk_ids(allids, nid, W, Hd1, k, impl=args.head, out=o_dense)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        dense["ours_full_vocab_us"] = ev0.elapsed_time(ev1) * 1e3 / reps
+        dense["best_dense_us"] = min(dense["cublas_topk_us"], dense["ours_full_vocab_us"])
+        dense["speedup_vs_dense"] = dense["best_dense_us"] / us_head
+
+    # roofline of the dominant kernel (the head call; algorithmic bytes SURVEY 8(d))
+    peak, peak_src = load_peaks()
+    alg_bytes = Wm * d * 2 + n * d * 2 + Wm * 4 + n * k * 8 + n * 4
+    achieved = alg_bytes / (us_head * 1e-6) / 1e9
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        us_cpu, sample = cpu_oracle_steps(cfg, n, k, args.cpu_sample_steps)
+        cpu = {"value": round(us_cpu, 1), "unit": "us/step", "cores": 1, "kind": "oracle", "sample": sample}
+
+    launches_per_step = 3  # state update + head contraction + top-k select
+    value = ms_total * 1e3 / (K * world)
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "us/step", "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": round(ms_total / K, 6), "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"{cfg['model']} draft head: V={V} d={d} |I|={Wm} (exact) n={n} k={k} batch=1 "
+                               f"per rank", "w_max": Wm, "n_nodes": n, "k": k, "head": args.head,
+                   "l2": f"inputs larger than L2: {R} rotating sequences with disjoint id pools "
+                         f"({R * Wm * d * 2 / 1e6:.0f} MB of distinct rows > 126 MB L2)",
+                   "parallelism": f"dp{world} (independent sequences, no collective)",
+                   "step": "state_update(60 draft + 3 verify ids) + draft_logits_topk"},
+        "breakdown": {"us_step": round(us_step, 3), "us_head_call": round(us_head, 3),
+                      "us_state_update": round(us_upd, 3), "head_gbps": round(achieved, 1)},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
+                     "kernel": "draft_logits_topk call (contraction + top-k select)",
+                     "alg_bytes_per_launch": alg_bytes},
+        "dense": {kk: (round(vv, 3) if isinstance(vv, float) else vv) for kk, vv in dense.items()},
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(us_e2e, 3), "unit": "us/step", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches_per_step * K,
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _mm_out_dtype_ok(torch):
+    try:
+        a = torch.zeros(1, 8, dtype=torch.bfloat16, device="cuda")
+        torch.mm(a, a.t(), out_dtype=torch.float32)
+        return True
+    except Exception:
+        return False
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,49 @@
+// Internal (non-ABI) launchers of the NanoSpec CUDA path.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace nanospec {
+
+cudaError_t launch_state_append(const StateView& sv, int seq0, int nseq, int reset,
+                                const int32_t* a, long long a_len, long long a_stride, int a_dedup,
+                                const int32_t* b, long long b_len, long long b_stride, int b_dedup,
+                                cudaStream_t stream);
+
+// Active rows of one head call: for sequence s, ids = ids_base + s*ids_stride,
+// n_active = *(nact_base + s*nact_stride).
+struct HeadProblem {
+  const uint16_t* w;        // bf16 bits [rows x ldw]
+  long long ldw;
+  int d;
+  const uint16_t* h;        // bf16 bits [batch x n x d]
+  int n;
+  int batch;
+  const int32_t* ids_base;
+  long long ids_stride;
+  const int32_t* nact_base;
+  long long nact_stride;
+  int max_ids;              // ids capacity per sequence (row stride of logits)
+  int n_shards;             // row(g) = g / n_shards
+  float* logits;            // fp32 [batch x n x max_ids]
+};
+
+// Phase 1 (a3+a4): gathered contraction into the fp32 logits staging buffer.
+cudaError_t launch_head_simt(const HeadProblem& p, int num_sms, cudaStream_t stream);
+// Tensor-core variant; returns cudaErrorNotSupported when the shape is not
+// covered (caller falls back to SIMT only if the caller asked for AUTO).
+cudaError_t launch_head_tc(const HeadProblem& p, void* scratch, size_t scratch_bytes, int num_sms,
+                           cudaStream_t stream);
+size_t head_tc_scratch_bytes(int batch, int max_ids, int n);
+
+// Phase 2 (a5): per (sequence, node) top-k by (value desc, id asc) + lse.
+cudaError_t launch_select_topk(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse,
+                               cudaStream_t stream);
+
+cudaError_t launch_merge_topk(const float* cand_logit, const int32_t* cand_id, const float* cand_lse,
+                              int n_shards, int n_rows, int k, float* out_logit, int32_t* out_id, float* out_lse,
+                              cudaStream_t stream);
+
+}  // namespace nanospec

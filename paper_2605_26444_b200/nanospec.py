@@ -1,0 +1,220 @@
+"""Thin Python binding over the C ABI (include/nanospec.h).
+
+Argument marshalling only: torch provides device memory and the current CUDA
+stream; every step of the path runs in the library's kernels.  Function names
+follow the ABI (and the paper's notation).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _native as N
+
+RULES = {"window": 0, "unique_fifo": 1}
+IMPLS = {"auto": 0, "simt": 1, "tc": 2}
+
+
+def _stream(device=None) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _need(t, dtype, name, device=None, numel=None):
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (there is no CPU path)")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if numel is not None and t.numel() != numel:
+        raise ValueError(f"{name} must have {numel} elements, got {t.numel()}")
+    return t
+
+
+def state_workspace_bytes(vocab, w_max, batch=1, rule="window", shard_rank=0, n_shards=1) -> int:
+    return int(N.lib().nanospec_state_workspace_bytes(vocab, w_max, batch, RULES[rule], shard_rank, n_shards))
+
+
+def head_scratch_bytes(batch, max_ids, n_nodes) -> int:
+    return int(N.lib().nanospec_head_scratch_bytes(batch, max_ids, n_nodes))
+
+
+class ActiveVocab:
+    """GPU-resident candidate-stream state for `batch` sequences (a1/a2).
+
+    I = Unique(Suffix(S, W_max)) (Eq. 5) kept as a bitmap + ascending id
+    list entirely in device memory."""
+
+    def __init__(self, vocab: int, w_max: int, batch: int = 1, rule: str = "window", shard_rank: int = 0,
+                 n_shards: int = 1, device=None):
+        self.vocab, self.w_max, self.batch, self.rule = vocab, w_max, batch, rule
+        self.shard_rank, self.n_shards = shard_rank, n_shards
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        nbytes = state_workspace_bytes(vocab, w_max, batch, rule, shard_rank, n_shards)
+        if nbytes == 0:
+            raise N.NanoSpecError(N.EINVAL, "nanospec_state_workspace_bytes")
+        self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+        off = (-self.workspace.data_ptr()) % 256
+        self._ws_ptr = self.workspace.data_ptr() + off
+        self._ws_bytes = nbytes
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            N.check(N.lib().nanospec_state_create(ctypes.byref(h), vocab, w_max, batch, RULES[rule], shard_rank,
+                                                  n_shards, self._ws_ptr, nbytes, _stream(self.device)),
+                    "nanospec_state_create")
+        self.handle = h.value
+        self.v_local = (vocab - shard_rank + n_shards - 1) // n_shards if n_shards > 1 else vocab
+        self.words = (self.v_local + 31) // 32
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            try:
+                N.lib().nanospec_state_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+    # a1: Eq. 3
+    def init(self, seq: int, prompt: torch.Tensor, prefill_topk: torch.Tensor | None = None):
+        _need(prompt, torch.int32, "prompt")
+        k_pre = 0
+        if prefill_topk is not None:
+            _need(prefill_topk, torch.int32, "prefill_topk")
+            L = prompt.numel()
+            if prefill_topk.numel() % max(L, 1):
+                raise ValueError("prefill_topk must be [L, k_pre]")
+            k_pre = prefill_topk.numel() // L if L else 0
+        st = N.lib().nanospec_state_init(self.handle, seq, _ptr(prompt), prompt.numel(),
+                                         _ptr(prefill_topk) if k_pre else None, k_pre, _stream(self.device))
+        N.check(st, "nanospec_state_init")
+
+    # a2: Eq. 4 + Eq. 5
+    def update(self, seq: int, draft: torch.Tensor | None, verify: torch.Tensor | None):
+        nd = 0 if draft is None else _need(draft, torch.int32, "draft").numel()
+        kv = 0 if verify is None else _need(verify, torch.int32, "verify").numel()
+        N.check(N.lib().nanospec_state_update(self.handle, seq, _ptr(draft) if nd else None, nd,
+                                              _ptr(verify) if kv else None, kv, _stream(self.device)),
+                "nanospec_state_update")
+
+    def update_batch(self, draft: torch.Tensor | None, verify: torch.Tensor | None):
+        nd = 0 if draft is None else _need(draft, torch.int32, "draft").numel() // self.batch
+        kv = 0 if verify is None else _need(verify, torch.int32, "verify").numel() // self.batch
+        N.check(N.lib().nanospec_state_update_batch(self.handle, _ptr(draft) if nd else None, nd,
+                                                    _ptr(verify) if kv else None, kv, _stream(self.device)),
+                "nanospec_state_update_batch")
+
+    def read(self, seq: int) -> dict:
+        """Synchronises the current stream; host copies of sequence `seq`'s state."""
+        import numpy as np
+        ids = np.empty(self.w_max, np.int32)
+        bm = np.empty(self.words, np.uint32)
+        ring = np.empty(self.w_max, np.int32)
+        n = ctypes.c_int32()
+        total = ctypes.c_int64()
+        err = ctypes.c_int32()
+        N.check(N.lib().nanospec_state_read(self.handle, seq, ids.ctypes.data, ctypes.byref(n), bm.ctypes.data,
+                                            ring.ctypes.data, ctypes.byref(total), ctypes.byref(err),
+                                            _stream(self.device)), "nanospec_state_read")
+        return dict(ids=ids[: n.value].copy(), n_active=n.value, bitmap=bm, ring=ring, total=total.value,
+                    err=err.value)
+
+    def check(self) -> int:
+        """Synchronises; returns the status (OK or EDEVICE)."""
+        st = N.lib().nanospec_state_check(self.handle, _stream(self.device))
+        if st not in (N.OK, N.EDEVICE):
+            N.check(st, "nanospec_state_check")
+        return st
+
+    def ids_ptr(self, seq: int) -> int:
+        return N.lib().nanospec_state_ids_ptr(self.handle, seq)
+
+    def n_active_ptr(self, seq: int) -> int:
+        return N.lib().nanospec_state_n_active_ptr(self.handle, seq)
+
+
+class HeadOutputs:
+    """Preallocated outputs + scratch for repeated (graph-captured) head calls."""
+
+    def __init__(self, batch: int, n_nodes: int, k: int, max_ids: int, device, lse: bool = True,
+                 debug_logits: bool = False):
+        self.batch, self.n_nodes, self.k, self.max_ids = batch, n_nodes, k, max_ids
+        self.topk_logit = torch.empty(batch, n_nodes, k, dtype=torch.float32, device=device)
+        self.topk_id = torch.empty(batch, n_nodes, k, dtype=torch.int32, device=device)
+        self.lse = torch.empty(batch, n_nodes, dtype=torch.float32, device=device) if lse else None
+        self.debug_logits = (torch.empty(batch, n_nodes, max_ids, dtype=torch.float32, device=device)
+                             if debug_logits else None)
+        nbytes = head_scratch_bytes(batch, max_ids, n_nodes)
+        if nbytes == 0:
+            raise N.NanoSpecError(N.EINVAL, "nanospec_head_scratch_bytes")
+        self.scratch = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+
+
+def draft_logits_topk(state: ActiveVocab, w_head: torch.Tensor, hidden: torch.Tensor, k: int, *,
+                      lse: bool = True, debug_logits: bool = False, impl: str = "auto",
+                      out: HeadOutputs | None = None):
+    """a3+a4+a5: top-k over W_head[I] h for every sequence and node.
+
+    hidden: bf16 [batch, n_nodes, d] (or [n_nodes, d] when batch == 1).
+    Returns (topk_logit [B,n,k] fp32, topk_id [B,n,k] int32, lse [B,n] or None,
+    debug_logits [B,n,W_max] or None)."""
+    _need(w_head, torch.bfloat16, "w_head")
+    _need(hidden, torch.bfloat16, "hidden")
+    d = w_head.shape[-1]
+    n_nodes = hidden.numel() // (state.batch * d)
+    if hidden.numel() != state.batch * n_nodes * d or hidden.shape[-1] != d:
+        raise ValueError("hidden must be [batch, n_nodes, d] with the weight's d")
+    if out is None:
+        out = HeadOutputs(state.batch, n_nodes, k, state.w_max, hidden.device, lse, debug_logits)
+    st = N.lib().nanospec_draft_logits_topk_ex(
+        state.handle, _ptr(w_head), d, w_head.stride(0), _ptr(hidden), n_nodes, k, _ptr(out.topk_logit),
+        _ptr(out.topk_id), _ptr(out.lse), _ptr(out.debug_logits), _ptr(out.scratch), out.scratch.numel(),
+        IMPLS[impl], _stream(hidden.device))
+    N.check(st, "nanospec_draft_logits_topk")
+    return out.topk_logit, out.topk_id, out.lse, out.debug_logits
+
+
+def logits_topk_ids(ids: torch.Tensor, n_ids: torch.Tensor, w_head: torch.Tensor, hidden: torch.Tensor, k: int, *,
+                    n_shards: int = 1, lse: bool = True, debug_logits: bool = False, impl: str = "auto",
+                    out: HeadOutputs | None = None):
+    """The head over an explicit ascending id list (e.g. [0, V): the dense
+    full-vocabulary head of Eq. 2).  n_ids: int32 [1] on device."""
+    _need(ids, torch.int32, "ids")
+    _need(n_ids, torch.int32, "n_ids", numel=1)
+    _need(w_head, torch.bfloat16, "w_head")
+    _need(hidden, torch.bfloat16, "hidden")
+    d = w_head.shape[-1]
+    n_nodes = hidden.numel() // d
+    if out is None:
+        out = HeadOutputs(1, n_nodes, k, ids.numel(), hidden.device, lse, debug_logits)
+    st = N.lib().nanospec_logits_topk_ids(
+        _ptr(ids), _ptr(n_ids), ids.numel(), n_shards, _ptr(w_head), d, w_head.stride(0), _ptr(hidden), n_nodes, k,
+        _ptr(out.topk_logit), _ptr(out.topk_id), _ptr(out.lse), _ptr(out.debug_logits), _ptr(out.scratch),
+        out.scratch.numel(), IMPLS[impl], _stream(hidden.device))
+    N.check(st, "nanospec_logits_topk_ids")
+    return out.topk_logit, out.topk_id, out.lse, out.debug_logits
+
+
+def merge_topk(cand_logit: torch.Tensor, cand_id: torch.Tensor, cand_lse: torch.Tensor | None, k: int):
+    """Exact top-k / lse over the union of vocab shards.
+    cand_logit/cand_id: [S, rows, k]; cand_lse: [S, rows]."""
+    _need(cand_logit, torch.float32, "cand_logit")
+    _need(cand_id, torch.int32, "cand_id")
+    S = cand_logit.shape[0]
+    rows = cand_logit.numel() // (S * k)
+    ol = torch.empty(rows, k, dtype=torch.float32, device=cand_logit.device)
+    oi = torch.empty(rows, k, dtype=torch.int32, device=cand_logit.device)
+    olse = None
+    if cand_lse is not None:
+        _need(cand_lse, torch.float32, "cand_lse")
+        olse = torch.empty(rows, dtype=torch.float32, device=cand_logit.device)
+    N.check(N.lib().nanospec_merge_topk(_ptr(cand_logit), _ptr(cand_id), _ptr(cand_lse), S, rows, k, _ptr(ol),
+                                        _ptr(oi), _ptr(olse), _stream(cand_logit.device)), "nanospec_merge_topk")
+    return ol, oi, olse
