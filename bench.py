@@ -237,7 +237,9 @@ def run_ours(args):
         r = s % R
         P.draft_logits_topk(states[r], W, Hs[r:r + 1], k, impl=args.head, out=outs[r])
 
-    stream = torch.cuda.current_stream(dev)
+    torch.cuda.synchronize()
+    stream = torch.cuda.Stream(dev)  # graphs must be captured on a non-default stream
+    torch.cuda.set_stream(stream)
     # warm-up (eager: also sets function attributes), then one captured warm-up graph
     for s in range(args.warmup):
         step(s)
