@@ -207,6 +207,14 @@ nanospec_status nanospec_merge_topk(const float* d_cand_logit, const int32_t* d_
                                     int32_t n_shards, int32_t n_rows, int32_t k, float* d_out_logit,
                                     int32_t* d_out_id, float* d_out_lse, cudaStream_t stream);
 
+/* Debug: phase trace.  d_buf = device uint64[ctas * 16] (ctas >= 256) or NULL
+ * (off, the default).  While set, the fused tensor-core head writes the
+ * %globaltimer (ns) of its phases, CTA b at d_buf[b*16 + e]: 0 start,
+ * 1 dependency resolved, 2 row pointers ready, 3 last load landed, 4 last MMA
+ * done, 5 epilogue done, 6 grid barrier passed, 7 top-k inputs staged,
+ * 8 top-k done.  Process-wide; not thread-safe; for profiling only. */
+nanospec_status nanospec_debug_set_trace(unsigned long long* d_buf, int32_t ctas);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -1,6 +1,8 @@
 """Builds libnanospec.so (the C-ABI library) in-tree with nvcc for sm_100a.
 
-    python -m paper_2605_26444_b200.build [--force]
+    python paper_2605_26444_b200/build.py [--force]
+
+(run by path: importing the package loads the library being built)
 
 No torch involvement: plain `nvcc -shared` over csrc/*.cu, static cudart.
 """

@@ -17,6 +17,11 @@ struct nanospec_state_s {
   size_t ws_bytes;
 };
 
+namespace nanospec {
+static unsigned long long* g_trace = nullptr;
+unsigned long long* trace_buffer() { return g_trace; }
+}  // namespace nanospec
+
 namespace {
 
 constexpr size_t kAlign = 256;
@@ -75,15 +80,17 @@ nanospec_status run_head(HeadProblem hp, int32_t k, float* d_topk_logit, int32_t
                          cudaStream_t stream) {
   const size_t lb = logits_bytes(hp.batch, hp.max_ids, hp.n);
   if (!d_scratch || scratch_bytes < nanospec_head_scratch_bytes(hp.batch, hp.max_ids, hp.n)) return NANOSPEC_EINVAL;
-  hp.logits = d_debug_logits ? d_debug_logits : (float*)d_scratch;
   char* rest = (char*)d_scratch + lb;
   size_t rest_bytes = scratch_bytes - lb;
-  cudaError_t e = cudaErrorNotSupported;
   if (impl == NANOSPEC_HEAD_TC || impl == NANOSPEC_HEAD_AUTO) {
-    e = launch_head_tc(hp, rest, rest_bytes, sm_count(), stream);
-    if (e == cudaErrorNotSupported && impl == NANOSPEC_HEAD_TC) return NANOSPEC_EUNSUPPORTED;
+    hp.logits = d_debug_logits;  // fused kernel: logits only if the caller wants them
+    cudaError_t e = launch_head_tc(hp, k, d_topk_logit, d_topk_id, d_lse, rest, rest_bytes, sm_count(), stream);
+    if (e == cudaSuccess) return NANOSPEC_OK;
+    if (e != cudaErrorNotSupported) return NANOSPEC_ECUDA;
+    if (impl == NANOSPEC_HEAD_TC) return NANOSPEC_EUNSUPPORTED;
   }
-  if (e == cudaErrorNotSupported) e = launch_head_simt(hp, sm_count(), stream);
+  hp.logits = d_debug_logits ? d_debug_logits : (float*)d_scratch;
+  cudaError_t e = launch_head_simt(hp, sm_count(), stream);
   if (e != cudaSuccess) return NANOSPEC_ECUDA;
   return cuda_status(launch_select_topk(hp, k, d_topk_logit, d_topk_id, d_lse, stream));
 }
@@ -267,6 +274,7 @@ nanospec_status nanospec_draft_logits_topk_ex(const nanospec_state st, const voi
   hp.max_ids = sv.w_max;
   hp.n_shards = sv.n_shards;
   hp.logits = nullptr;
+  hp.trace = trace_buffer();
   return run_head(hp, k, d_topk_logit, d_topk_id, d_lse, d_debug_logits, d_scratch, scratch_bytes, impl, stream);
 }
 
@@ -304,7 +312,14 @@ nanospec_status nanospec_logits_topk_ids(const int32_t* d_ids, const int32_t* d_
   hp.max_ids = max_ids;
   hp.n_shards = n_shards;
   hp.logits = nullptr;
+  hp.trace = trace_buffer();
   return run_head(hp, k, d_topk_logit, d_topk_id, d_lse, d_debug_logits, d_scratch, scratch_bytes, impl, stream);
+}
+
+nanospec_status nanospec_debug_set_trace(unsigned long long* d_buf, int32_t ctas) {
+  if (d_buf && ctas < 256) return NANOSPEC_EINVAL;
+  g_trace = d_buf;
+  return NANOSPEC_OK;
 }
 
 nanospec_status nanospec_merge_topk(const float* d_cand_logit, const int32_t* d_cand_id, const float* d_cand_lse,

@@ -97,4 +97,16 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
 __device__ __forceinline__ float bf16lo(uint32_t u) { return __uint_as_float(u << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
 
+// Optional phase trace (debug): when `trace` is non-null, CTA b writes the
+// %globaltimer (ns) of phase e to trace[b * kTraceSlots + e].
+constexpr int kTraceSlots = 16;
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_mark(unsigned long long* trace, int e) {
+  if (trace) trace[(long long)blockIdx.x * kTraceSlots + e] = globaltimer();
+}
+
 }  // namespace nanospec

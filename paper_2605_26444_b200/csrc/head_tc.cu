@@ -1,30 +1,37 @@
-// a3+a4 on the 5th-generation tensor cores (tcgen05.mma, accumulators in TMEM).
+// a3+a4+a5 in ONE kernel on the 5th-generation tensor cores (tcgen05.mma,
+// accumulators in TMEM):
 //
-//   logits[b][i][j] = sum_c W[row(ids_b[j])][c] * H[b][i][c]     (Eq. 2 on I)
+//   z'[b][i][j] = sum_c W[row(ids_b[j])][c] * H[b][i][c]     (Eq. 2 on I)
+//   then per (b, i) the top-k of z' by (value desc, id asc) + lse
 //
-// The paper gathers the active rows into a dense repack buffer on a copy
-// stream and then runs a dense GEMM.  Here the gather is fused into
-// the contraction's load stage instead: each 128-row tile of active rows is
-// pulled straight from W_head with 16-byte cp.async into 128B-swizzled shared
-// memory (the UMMA K-major SW128 layout), so the weight bytes cross HBM exactly
-// once and no repack buffer is written.
+// Gather.  The paper repacks the active rows into a dense buffer on a copy
+// stream before a dense GEMM.  Here the gather is fused into the
+// contraction's load stage: each 128-row tile of active rows is pulled
+// straight from W_head with 16-byte cp.async into 128B-swizzled shared memory
+// (the UMMA K-major SW128 layout), so weight bytes cross HBM exactly once.
 //
-// Tile: UMMA M = 128 active rows (A operand), N = NT >= n draft nodes (B
-// operand, zero-padded), K = 64 per stage (one 128-byte swizzle atom).  D lives
-// in TMEM (NT fp32 columns x 128 lanes).
+// Contraction.  UMMA M = 128 active rows (A), N = NT >= n nodes (B, zero
+// padded), K = 64 per pipeline stage; D in TMEM (NT fp32 columns).  T =
+// sum_b ceil(n_active_b / 128) tiles are read from device memory (no host
+// sync); every tile is split along K into S = max(1, floor(#SMs / T)) uniform
+// chunks so that ~all SMs stream.  Each (tile, chunk) unit writes its fp32
+// partial tile to L2-resident scratch.
 //
-// Work split: T = sum_b ceil(n_active_b / 128) tiles are read from device
-// memory (no host sync).  With T < #SMs every tile is split along K into
-// S = floor(#SMs / T) uniform chunks (one unit per CTA); partial tiles are
-// reduced in a fixed order (split 0, 1, ..., S-1) by the S CTAs of the tile,
-// each reducing a slice of its rows, so equal rows give bit-equal logits.  With
-// T >= #SMs, S = 1 and CTAs loop over whole tiles.  The kernel is launched
-// cooperatively (all CTAs co-resident), which makes the split-K spin-wait safe.
+// Top-k, two levels spread over all CTAs.  Level 1: as soon as the S partials
+// of a tile are written (per-tile arrival counter; the launch is cooperative so
+// all CTAs are co-resident and the spin is safe), the tile's S CTAs split its
+// (tile, node) pairs; one warp per pair sums the S partials of the 128 rows in
+// split order (fixed order -> equal rows give bit-equal logits) and keeps the
+// pair's exact top-k (k arg-max rounds over (value desc, id asc) packed into
+// 64-bit keys) plus (max, sum exp) for the lse.  Level 2, after one grid
+// barrier: one CTA per (sequence, node) merges the ceil(|I|/128) * k level-1
+// candidates the same way and combines the lse partials.
 //
-// Warp roles (160 threads): warps 0-3 load (cp.async) and run the epilogue
-// (tcgen05.ld, one TMEM lane = one active row per thread); warp 4 allocates
-// TMEM and one elected lane issues the MMAs.
-#include <cuda.h>
+// Warp roles (544 threads): warps 0-15 load (cp.async) and drain TMEM (warp w
+// reads TMEM lanes 32*(w%4).. and a quarter of the columns); warp 16 allocates
+// TMEM and one lane issues the MMAs.  All 17 warps run the top-k phase (enough
+// warps per scheduler to hide shared-memory and shuffle latencies).
+#include <math.h>
 
 #include "common.cuh"
 #include "internal.h"
@@ -35,16 +42,23 @@ namespace {
 
 constexpr int kBM = 128;          // active rows per tile (UMMA M)
 constexpr int kBK = 64;           // K per stage (bf16 -> 128 bytes)
-constexpr int kLoadWarps = 4;
-constexpr int kThreads = (kLoadWarps + 1) * 32;
-constexpr int kSmemBudget = 200 * 1024;
+constexpr int kLoadWarps = 16;    // loaders / epilogue / top-k
+constexpr int kLoaders = kLoadWarps * 32;
+constexpr int kThreads = kLoaders + 32;   // + one MMA-issue warp
+constexpr int kWarps = kThreads / 32;
+constexpr int kSmemBudget = 192 * 1024;
 constexpr int kMaxSMs = 256;
+constexpr int kCandCap = 1024;    // candidates kept for the exact ranking
+constexpr int kMaxK = 32;
 
 struct TcArgs {
   HeadProblem p;
-  float* part;          // [units][NT][128] fp32 split-K partials
-  unsigned* arrive;     // [max tiles] split-K arrival counters (zero between launches)
-  unsigned* done;       // [max tiles]
+  float* part;                 // [units][NT][128] fp32 partial tiles (split-K)
+  unsigned* counters;          // [0] grid arrive, [1] grid done (zero between launches)
+  float* topk_logit;           // [batch][n][k]
+  int32_t* topk_id;
+  float* lse;                  // [batch][n] or null
+  int k;
   int max_tiles;
 };
 
@@ -52,15 +66,12 @@ struct TcArgs {
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
 }
-
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
-
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t done = 0;
   do {
@@ -73,40 +84,28 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "memory");
   } while (!done);
 }
-
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-// K-major, 128B-swizzled UMMA shared-memory descriptor (SM100 format):
-// start>>4 [0,14), LBO>>4 [16,30) (unused for SW128 K-major: 1), SBO>>4 [32,46)
-// = 1024 B between 8-row groups, version 1 at [46,48), layout SWIZZLE_128B (2)
-// at [61,64).
+// K-major, 128B-swizzled UMMA shared-memory descriptor (SM100): start>>4
+// [0,14), LBO>>4 [16,30) (unused for SW128 K-major: 1), SBO>>4 [32,46) = 1024 B
+// between 8-row groups, version 1 at [46,48), layout SWIZZLE_128B (2) at [61,64).
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)1u << 16;
-  d |= (uint64_t)(1024u >> 4) << 32;
-  d |= (uint64_t)1u << 46;
-  d |= (uint64_t)2u << 61;
-  return d;
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1u << 16) | ((uint64_t)(1024u >> 4) << 32) |
+         ((uint64_t)1u << 46) | ((uint64_t)2u << 61);
 }
-
-// Instruction descriptor, kind::f16: D fp32, A/B bf16, both K-major, N, M.
+// Instruction descriptor, kind::f16: D fp32 [4,6)=1, A bf16 [7,10)=1, B bf16
+// [10,13)=1, both K-major, N>>3 at [17,23), M>>4 at [24,29).
 __host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
-
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                           uint32_t accumulate) {
   asm volatile(
@@ -116,12 +115,10 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint6
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                : "memory");
 }
-
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   uint32_t r[16];
   asm volatile(
@@ -133,89 +130,273 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
-
 __device__ __forceinline__ uint32_t ld_acquire(const unsigned* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 // ------------------------------------------------------------------ work split
-struct Split {
-  int tiles;  // total row tiles over all sequences
-  int S;      // K chunks per tile
-  int units;  // tiles * S
-};
-
-__device__ __forceinline__ Split compute_split(const HeadProblem& p, int grid, int kb) {
-  Split s;
-  int t = 0;
-  for (int b = 0; b < p.batch; ++b) {
-    int m = p.nact_base[(long long)b * p.nact_stride];
-    m = m < 0 ? 0 : (m > p.max_ids ? p.max_ids : m);
-    t += (m + kBM - 1) / kBM;
-  }
-  s.tiles = t;
-  s.S = t >= grid || t == 0 ? 1 : min(kb, grid / t);
-  s.units = t * s.S;
-  return s;
+__device__ __forceinline__ int clamp_nact(const HeadProblem& p, int b) {
+  int m = p.nact_base[(long long)b * p.nact_stride];
+  return m < 0 ? 0 : (m > p.max_ids ? p.max_ids : m);
 }
+__device__ __forceinline__ int batch_m0(const HeadProblem& p) { return p.batch > 0 ? clamp_nact(p, 0) : 0; }
 
-// tile index -> (sequence, first row, valid rows)
-__device__ __forceinline__ void locate_tile(const HeadProblem& p, int tile, int& seq, int& row0, int& rows) {
-  int t = tile;
-  for (int b = 0; b < p.batch; ++b) {
-    int m = p.nact_base[(long long)b * p.nact_stride];
-    m = m < 0 ? 0 : (m > p.max_ids ? p.max_ids : m);
-    int nt = (m + kBM - 1) / kBM;
-    if (t < nt) {
-      seq = b;
-      row0 = t * kBM;
-      rows = min(kBM, m - row0);
-      return;
-    }
-    t -= nt;
-  }
-  seq = 0;
-  row0 = 0;
-  rows = 0;
-}
+
 
 template <int NT>
 struct Cfg {
-  static constexpr int kABytes = kBM * kBK * 2;   // 16 KB
-  static constexpr int kBBytes = NT * kBK * 2;    // NT * 128 B
+  static constexpr int kABytes = kBM * kBK * 2;  // 16 KB
+  static constexpr int kBBytes = NT * kBK * 2;   // NT * 128 B
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStages = (kSmemBudget / kStageBytes) > 8 ? 8 : (kSmemBudget / kStageBytes);
   static constexpr int kTmemCols = NT < 32 ? 32 : NT;
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 2048 /*barriers, row table*/;
+  static constexpr int kStageArea = kStages * kStageBytes;
+  static constexpr int kSmemBytes = kStageArea + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(2 * kStages + 3 <= 30, "barrier area");
+  static constexpr int kHChunks = NT * 8;                 // 16-B chunks of one H stage
+  static constexpr int kColGroups = NT / 16 < 4 ? NT / 16 : 4;  // epilogue column groups
 };
+
+struct TopkSmem {
+  float wthr[kWarps];
+  float wmax[kWarps];
+  float wsum[kWarps];
+  int wcnt[kWarps];
+  int woff[kWarps + 1];
+  int nbest;
+  float best_v[kMaxK];
+  int32_t best_g[kMaxK];
+};
+
+__device__ __forceinline__ bool ranks_before(float va, int32_t ga, float vb, int32_t gb) {
+  const uint32_t ka = float_key(va), kb = float_key(vb);
+  return ka > kb || (ka == kb && ga < gb);
+}
+
+// Top-k + lse of one (sequence, node), the whole CTA.  Logits are the sums of
+// the S split partials (fixed split order) of every active row, gathered with
+// all loads of a thread in flight at once, staged (value, id) in shared memory;
+// then T = max over warps of the k-th largest lane maximum (a lower bound on
+// the k-th largest value), the values >= T are compacted and ranked by
+// counting against each other (value desc, id asc).
+template <int NT>
+__device__ void topk_node(const TcArgs& a, int seq, int node, int tile_base, int S, uint8_t* smem, TopkSmem& sh) {
+  using C = Cfg<NT>;
+  const HeadProblem& p = a.p;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int m = clamp_nact(p, seq);
+  const int k = a.k;
+  const int32_t* ids = p.ids_base + (long long)seq * p.ids_stride;
+  const long long ob = ((long long)seq * p.n + node) * k;
+  // shared memory: [vals cap][gids cap][cand_v kCandCap][cand_g kCandCap]
+  constexpr int kCap = ((C::kStageArea - 2 * kCandCap * 4) / 8) & ~127;
+  float* vals = reinterpret_cast<float*>(smem);
+  int32_t* gids = reinterpret_cast<int32_t*>(smem + (size_t)kCap * 4);
+  float* cv = reinterpret_cast<float*>(smem + (size_t)kCap * 8);
+  int32_t* cg = reinterpret_cast<int32_t*>(smem + (size_t)kCap * 8 + kCandCap * 4);
+  if (tid == 0) sh.nbest = 0;
+  float run_max = -INFINITY, run_sum = 0.f;  // online lse over chunks (block-uniform)
+  for (int c0 = 0; c0 < m; c0 += kCap) {
+    const int mc = min(kCap, m - c0);
+    const int ng = (mc + 3) / 4;  // float4 row groups (never straddle a 128-row tile)
+    __syncthreads();              // previous chunk's readers are done
+    // 1. gather + sum: thread t takes groups t, t + kThreads, ... two at a time
+    float lmax = -INFINITY;
+    for (int g0 = tid; g0 < ng; g0 += 2 * kThreads) {
+      float4 acc[2];
+      int4 gi[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        acc[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int g = g0 + h * kThreads;
+        if (g < ng) {
+          const int j = c0 + 4 * g;  // first row of the group
+          const float* src = a.part + ((long long)(tile_base + j / kBM) * S * NT + node) * kBM + (j % kBM);
+          for (int s0 = 0; s0 < S; s0 += 8) {
+            float4 x[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (s0 + q < S) x[q] = __ldcg(reinterpret_cast<const float4*>(src + (long long)(s0 + q) * NT * kBM));
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (s0 + q < S) { acc[h].x += x[q].x; acc[h].y += x[q].y; acc[h].z += x[q].z; acc[h].w += x[q].w; }
+          }
+          if (((p.ids_stride | j) & 3) == 0 && j + 3 < m) {
+            gi[h] = __ldg(reinterpret_cast<const int4*>(ids + j));
+          } else {
+            gi[h].x = ids[min(j, m - 1)];
+            gi[h].y = ids[min(j + 1, m - 1)];
+            gi[h].z = ids[min(j + 2, m - 1)];
+            gi[h].w = ids[min(j + 3, m - 1)];
+          }
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int g = g0 + h * kThreads;
+        if (g < ng) {
+          const int jj = 4 * g;
+          const float v[4] = {acc[h].x, acc[h].y, acc[h].z, acc[h].w};
+          const int32_t gg[4] = {gi[h].x, gi[h].y, gi[h].z, gi[h].w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if (jj + i < mc) {
+              vals[jj + i] = v[i];
+              gids[jj + i] = gg[i];
+              lmax = fmaxf(lmax, v[i]);
+              if (p.logits) p.logits[((long long)seq * p.n + node) * p.max_ids + c0 + jj + i] = v[i];
+            }
+          }
+        }
+      }
+    }
+    if (tid == 0 && c0 == 0) trace_mark(p.trace, 7);  // logits gathered
+    // 2. per-warp k-th largest lane maximum (rank by counting over the 32 lanes)
+    {
+      int rank = 0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float o = __shfl_sync(0xffffffffu, lmax, j);
+        rank += (o > lmax || (o == lmax && j < lane)) ? 1 : 0;
+      }
+      const unsigned sel = __ballot_sync(0xffffffffu, rank == min(k, 32) - 1);
+      const float kth = __shfl_sync(0xffffffffu, lmax, __ffs(sel) - 1);
+      float wm = lmax;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+      if (lane == 0) { sh.wthr[warp] = kth; sh.wmax[warp] = wm; }
+    }
+    __syncthreads();
+    float T = -INFINITY, cmax = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) { T = fmaxf(T, sh.wthr[w]); cmax = fmaxf(cmax, sh.wmax[w]); }
+    const int nprev = sh.nbest;
+    if (nprev == k) T = fmaxf(T, sh.best_v[k - 1]);
+    if (tid == 0 && c0 == 0) trace_mark(p.trace, 9);  // threshold
+    // 3. count candidates >= T per warp (same element order as the compaction
+    //    below) and the chunk's sum exp(v - cmax)
+    int wc = 0;
+    float es = 0.f;
+    for (int base = warp * 32; base < mc; base += kThreads) {
+      const int jj = base + lane;
+      const float v = jj < mc ? vals[jj] : -INFINITY;
+      wc += __popc(__ballot_sync(0xffffffffu, jj < mc && v >= T));
+      if (jj < mc) es += __expf(v - cmax);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
+    if (lane == 0) { sh.wcnt[warp] = wc; sh.wsum[warp] = es; }
+    __syncthreads();
+    if (warp == 0) {
+      const int c = lane < kWarps ? sh.wcnt[lane] : 0;
+      int x = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane < kWarps) sh.woff[lane] = nprev + x - c;
+      if (lane == 31) sh.woff[kWarps] = nprev + x;
+    }
+    float csum = 0.f;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) csum += sh.wsum[w];
+    const float nm = fmaxf(run_max, cmax);
+    run_sum = (run_max == -INFINITY ? 0.f : run_sum * __expf(run_max - nm)) + csum * __expf(cmax - nm);
+    run_max = nm;
+    __syncthreads();
+    if (sh.woff[kWarps] > kCandCap) {
+      // Degenerate ties (e.g. h = 0): more than kCandCap values >= T.  Exact
+      // but slow: one thread walks the chunk in row order (= ascending id)
+      // keeping a sorted best-k list; ties keep the earlier (smaller) id.
+      if (tid == 0) {
+        int nb = sh.nbest;
+        for (int jj = 0; jj < mc; ++jj) {
+          const float v = vals[jj];
+          const int32_t g = gids[jj];
+          if (nb == k && !ranks_before(v, g, sh.best_v[k - 1], sh.best_g[k - 1])) continue;
+          int pos = nb < k ? nb : k - 1;
+          while (pos > 0 && ranks_before(v, g, sh.best_v[pos - 1], sh.best_g[pos - 1])) {
+            sh.best_v[pos] = sh.best_v[pos - 1];
+            sh.best_g[pos] = sh.best_g[pos - 1];
+            --pos;
+          }
+          sh.best_v[pos] = v;
+          sh.best_g[pos] = g;
+          if (nb < k) ++nb;
+        }
+        sh.nbest = nb;
+      }
+      __syncthreads();
+      continue;
+    }
+    const int tot = sh.woff[kWarps];
+    if (tid == 0 && c0 == 0) trace_mark(p.trace, 10);  // counted
+    // 4. compact: previous best first, then this chunk's candidates
+    if (tid < nprev) { cv[tid] = sh.best_v[tid]; cg[tid] = sh.best_g[tid]; }
+    {
+      int off = sh.woff[warp];
+      for (int base = warp * 32; base < mc; base += kThreads) {
+        const int jj = base + lane;
+        const bool c = jj < mc && vals[jj] >= T;
+        const unsigned bal = __ballot_sync(0xffffffffu, c);
+        const int slot = off + __popc(bal & ((1u << lane) - 1u));
+        if (c) { cv[slot] = vals[jj]; cg[slot] = gids[jj]; }
+        off += __popc(bal);
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && c0 == 0) trace_mark(p.trace, 11);  // compacted
+    // 5. rank by counting; the k winners land in best[rank]
+    for (int e = tid; e < tot; e += kThreads) {
+      const float ve = cv[e];
+      const int32_t ge = cg[e];
+      int r = 0;
+      for (int f = 0; f < tot; ++f) r += ranks_before(cv[f], cg[f], ve, ge) ? 1 : 0;
+      if (r < k) { sh.best_v[r] = ve; sh.best_g[r] = ge; }
+    }
+    __syncthreads();
+    if (tid == 0) sh.nbest = min(k, tot);
+    if (tid == 0 && c0 == 0) trace_mark(p.trace, 12);  // ranked
+    __syncthreads();
+  }
+  if (tid < k) {
+    const bool ok = tid < sh.nbest;
+    a.topk_logit[ob + tid] = ok ? sh.best_v[tid] : -INFINITY;
+    a.topk_id[ob + tid] = ok ? sh.best_g[tid] : -1;
+  }
+  if (a.lse && tid == 0)
+    a.lse[(long long)seq * p.n + node] = run_max == -INFINITY ? -INFINITY : run_max + logf(run_sum);
+}
 
 template <int NT>
 __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
   using C = Cfg<NT>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* tiles_base = smem;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-B aligned view that keeps the shared address space visible to the compiler
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStageArea);
   // bars[0..S) full, [S..2S) empty, [2S] tmem_full, [2S+1] tmem_empty
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::kStages + 2);
-  const uint16_t** row_ptr = reinterpret_cast<const uint16_t**>(tmem_slot + 2);  // [128]
+  __shared__ int sh_tiles, sh_S, sh_m0;
+  __shared__ TopkSmem tsh;
 
   const HeadProblem& p = a.p;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int KB = p.d / kBK;
+  const int G = gridDim.x;
 
-  const Split sp = compute_split(p, gridDim.x, KB);
-
+  if (tid == 0) trace_mark(p.trace, 0);  // start
   if (tid == 0) {
     for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(smem_u32(&bars[s]), kLoadWarps * 32);          // full: every loader thread arrives
-      mbar_init(smem_u32(&bars[C::kStages + s]), 1);           // empty: one tcgen05.commit
+      mbar_init(smem_u32(&bars[s]), kLoaders);          // full: every loader thread arrives
+      mbar_init(smem_u32(&bars[C::kStages + s]), 1);    // empty: one tcgen05.commit
     }
-    mbar_init(smem_u32(&bars[2 * C::kStages]), 1);             // tmem_full
-    mbar_init(smem_u32(&bars[2 * C::kStages + 1]), kLoadWarps * 32);  // tmem_empty
+    mbar_init(smem_u32(&bars[2 * C::kStages]), 1);              // tmem_full
+    mbar_init(smem_u32(&bars[2 * C::kStages + 1]), kLoaders);   // tmem_empty
     fence_proxy_async();
   }
   if (warp == kLoadWarps) {
@@ -223,97 +404,136 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
                  "n"(C::kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  // Everything above overlaps the previous kernel (programmatic dependent
+  // launch); the state it produced (n_active, ids) is read only after this.
+  pdl_wait();
+  if (tid == 0) trace_mark(p.trace, 1);  // dependency resolved
+
+  // Loader pattern: thread t moves 16-B chunk (t & 7) of tile rows lr and
+  // lr + 64 (lr = t >> 3) of every W stage, and of H rows lr + 64 i < NT.
+  const int lr = tid >> 3;
+  const uint32_t swz = (uint32_t)(((tid & 7) ^ (lr & 7)) << 4);
+  // Speculative first unit, assuming every sequence holds max_ids active rows:
+  // its id loads go out together with the n_active reads (re-issued below if
+  // the guess is wrong).
+  const int tps_g = (p.max_ids + kBM - 1) / kBM;
+  const int tiles_g = p.batch * tps_g;
+  const int S_g = (tiles_g >= G) ? 1 : min(KB, G / tiles_g);
+  int32_t gid_pre[2] = {0, 0};
+  if (warp < kLoadWarps && (int)blockIdx.x < tiles_g * S_g) {
+    const int tg = blockIdx.x / S_g;
+    const int32_t* idp = p.ids_base + (long long)(tg / tps_g) * p.ids_stride + (tg % tps_g) * kBM;
+    const int lim = p.max_ids - (tg % tps_g) * kBM - 1;
+    gid_pre[0] = __ldg(idp + min(lr, lim));
+    gid_pre[1] = __ldg(idp + min(lr + 64, lim));
+  }
+  if (warp == 0) {
+    int t = 0, m0 = 0;
+    for (int b = lane; b < p.batch; b += 32) {
+      const int m = clamp_nact(p, b);
+      if (b == 0) m0 = m;
+      t += (m + kBM - 1) / kBM;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) {
+      sh_tiles = t;
+      sh_S = (t >= G || t == 0) ? 1 : min(KB, G / t);
+      sh_m0 = m0;
+    }
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const int tiles = sh_tiles, S = sh_S, units = tiles * S;
+  const bool guess_ok = (S == S_g && tiles == tiles_g);
   constexpr uint32_t idesc = make_idesc(kBM, NT);
 
-  int it = 0;      // pipeline iteration counter across units (same sequence in every role)
+  int it = 0;      // pipeline iteration counter across units
   int local = 0;   // units processed by this CTA
-  for (int u = blockIdx.x; u < sp.units; u += gridDim.x, ++local) {
-    const int tile = u / sp.S, split = u - (u / sp.S) * sp.S;
-    const int kb0 = split * KB / sp.S, kb1 = (split + 1) * KB / sp.S;
+  int seq = 0, seq_tile0 = 0, seq_m = sh_m0;  // tile -> sequence walk (units are tile-major)
+  for (int u = blockIdx.x; u < units; u += G, ++local) {
+    const int tile = u / S, split = u - (u / S) * S;
+    while (tile - seq_tile0 >= (seq_m + kBM - 1) / kBM) {  // advance to the tile's sequence
+      seq_tile0 += (seq_m + kBM - 1) / kBM;
+      ++seq;
+      seq_m = clamp_nact(p, seq);
+    }
+    const int row0 = (tile - seq_tile0) * kBM;
+    const int rows = min(kBM, seq_m - row0);
+    const int kb0 = split * KB / S, kb1 = (split + 1) * KB / S;
     const int nk = kb1 - kb0;
-    int seq, row0, rows;
-    locate_tile(p, tile, seq, row0, rows);
 
     if (warp < kLoadWarps) {
       // ---------------- producers: gather rows of W_head + H into SW128 stages
-      asm volatile("bar.sync 1, %0;" ::"n"(kLoadWarps * 32));  // previous unit done with row_ptr
-      if (tid < kBM) {
-        const int j = row0 + tid;
-        const uint16_t* rp = nullptr;
-        if (tid < rows) {
-          const int32_t g = p.ids_base[(long long)seq * p.ids_stride + j];
-          const long long r = p.n_shards > 1 ? g / p.n_shards : g;
-          rp = p.w + r * p.ldw;
-        }
-        row_ptr[tid] = rp;
+      int32_t gid[2];
+      if (local == 0 && guess_ok) {
+        gid[0] = gid_pre[0];
+        gid[1] = gid_pre[1];
+      } else {
+        const int32_t* idp = p.ids_base + (long long)seq * p.ids_stride + row0;
+        gid[0] = __ldg(idp + min(lr, rows - 1));
+        gid[1] = __ldg(idp + min(lr + 64, rows - 1));
       }
-      asm volatile("bar.sync 1, %0;" ::"n"(kLoadWarps * 32));
-      const uint16_t* hseq = p.h + (long long)seq * p.n * p.d;
+      const uint16_t* rp[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const long long row = p.n_shards > 1 ? gid[i] / p.n_shards : gid[i];
+        rp[i] = (lr + 64 * i < rows) ? p.w + row * p.ldw + (tid & 7) * 8 : nullptr;
+      }
+      const uint16_t* hp = p.h + (long long)seq * p.n * p.d + (tid & 7) * 8;
+      if (tid == 0 && local == 0) trace_mark(p.trace, 2);  // row pointers ready, first loads next
       for (int q = 0; q < nk + C::kStages - 1; ++q) {
         if (q < nk) {
           const int g_it = it + q;
           const int stage = g_it % C::kStages;
           if (g_it >= C::kStages) mbar_wait(smem_u32(&bars[C::kStages + stage]), ((g_it / C::kStages) - 1) & 1);
-          const uint32_t sA = smem_u32(tiles_base + stage * C::kStageBytes);
+          const uint32_t sA = smem_u32(smem + stage * C::kStageBytes);
           const uint32_t sB = sA + C::kABytes;
           const int kcol = (kb0 + q) * kBK;
 #pragma unroll
-          for (int i = 0; i < (kBM * 8) / (kLoadWarps * 32); ++i) {
-            const int ch = i * (kLoadWarps * 32) + tid;
-            const int r = ch >> 3, c = ch & 7;
-            const uint16_t* rp = row_ptr[r];
-            const uint32_t dst = sA + r * 128 + ((c ^ (r & 7)) << 4);
-            cp_async16(dst, rp ? (const void*)(rp + kcol + c * 8) : (const void*)p.w, rp ? 16u : 0u);
-          }
+          for (int i = 0; i < 2; ++i)
+            cp_async16(sA + (lr + 64 * i) * 128 + swz, rp[i] ? (const void*)(rp[i] + kcol) : (const void*)p.w,
+                       rp[i] ? 16u : 0u);
 #pragma unroll
-          for (int i = 0; i < (NT * 8 + kLoadWarps * 32 - 1) / (kLoadWarps * 32); ++i) {
-            const int ch = i * (kLoadWarps * 32) + tid;
-            if (ch < NT * 8) {
-              const int r = ch >> 3, c = ch & 7;
-              const bool ok = r < p.n;
-              const uint32_t dst = sB + r * 128 + ((c ^ (r & 7)) << 4);
-              cp_async16(dst, ok ? (const void*)(hseq + (long long)r * p.d + kcol + c * 8) : (const void*)p.h,
-                         ok ? 16u : 0u);
-            }
+          for (int i = 0; i < (C::kHChunks + kLoaders - 1) / kLoaders; ++i) {
+            const int hr = lr + 64 * i;
+            if (hr < NT)
+              cp_async16(sB + hr * 128 + swz, hr < p.n ? (const void*)(hp + (long long)hr * p.d + kcol) : (const void*)p.h,
+                         hr < p.n ? 16u : 0u);
           }
         }
         cp_async_commit();
         if (q >= C::kStages - 1) {
-          const int jq = q - (C::kStages - 1);
           cp_async_wait<C::kStages - 1>();
           fence_proxy_async();
-          mbar_arrive(smem_u32(&bars[(it + jq) % C::kStages]));
+          mbar_arrive(smem_u32(&bars[(it + q - (C::kStages - 1)) % C::kStages]));
         }
       }
-      // ---------------- epilogue: TMEM -> registers -> logits or split-K partials
+      if (tid == 0 && local == 0) trace_mark(p.trace, 3);  // all loads issued and landed
+      // ---------------- epilogue: TMEM -> registers -> partial tile (L2)
       mbar_wait(smem_u32(&bars[2 * C::kStages]), local & 1);
       tc_fence_after();
-      const int r = warp * 32 + lane;  // TMEM lane == tile row
-      const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
+      if (tid == 0 && local == 0) trace_mark(p.trace, 4);  // last MMA done
+      const int lg = warp & 3, cgp = warp >> 2;   // TMEM lane group, column group
+      const int r = lg * 32 + lane;               // TMEM lane == tile row
+      const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16);
+      float* dst = a.part + (long long)u * NT * kBM + r;
+      if (cgp < C::kColGroups) {
 #pragma unroll 1
-      for (int c0 = 0; c0 < NT && c0 < p.n; c0 += 16) {
-        float v[16];
-        tmem_ld16(taddr + c0, v);
-        if (sp.S == 1) {
-          if (r < rows) {
-#pragma unroll
-            for (int c = 0; c < 16; ++c)
-              if (c0 + c < p.n) p.logits[((long long)seq * p.n + c0 + c) * p.max_ids + row0 + r] = v[c];
-          }
-        } else {
+        for (int c0 = cgp * 16; c0 < NT && c0 < p.n; c0 += 16 * C::kColGroups) {
+          float v[16];
+          tmem_ld16(taddr + c0, v);
 #pragma unroll
           for (int c = 0; c < 16; ++c)
-            if (c0 + c < p.n) a.part[((long long)u * NT + c0 + c) * kBM + r] = v[c];
+            if (c0 + c < p.n) __stcg(dst + (c0 + c) * kBM, v[c]);
         }
       }
       tc_fence_before();
       mbar_arrive(smem_u32(&bars[2 * C::kStages + 1]));
     } else {
-      // ---------------- MMA issuer (warp 4, one lane)
+      // ---------------- MMA issuer (warp 16, one lane)
       if (local > 0) {
         mbar_wait(smem_u32(&bars[2 * C::kStages + 1]), (local - 1) & 1);
         tc_fence_after();
@@ -324,12 +544,11 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
         mbar_wait(smem_u32(&bars[stage]), (g_it / C::kStages) & 1);
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t sA = smem_u32(tiles_base + stage * C::kStageBytes);
+          const uint32_t sA = smem_u32(smem + stage * C::kStageBytes);
           const uint32_t sB = sA + C::kABytes;
 #pragma unroll
-          for (int kk = 0; kk < kBK / 16; ++kk) {
+          for (int kk = 0; kk < kBK / 16; ++kk)
             umma_bf16(tmem, sw128_desc(sA + kk * 32), sw128_desc(sB + kk * 32), idesc, (q | kk) ? 1u : 0u);
-          }
           umma_commit(smem_u32(&bars[C::kStages + stage]));
           if (q == nk - 1) umma_commit(smem_u32(&bars[2 * C::kStages]));
         }
@@ -337,39 +556,49 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
       }
     }
     it += nk;
+  }
 
-    if (sp.S > 1) {
-      // ---------------- fixed-order split-K reduction, distributed over the tile's CTAs
-      __threadfence();
-      __syncthreads();
-      if (tid == 0) {
-        atomicAdd(&a.arrive[tile], 1u);
-        while (ld_acquire(&a.arrive[tile]) < (unsigned)sp.S) __nanosleep(64);
+  // ---------------- grid barrier: every partial tile written
+  if (tid == 0) trace_mark(p.trace, 5);  // epilogue done
+  __threadfence();
+  tc_fence_before();
+  __syncthreads();
+  const int tasks = p.batch * p.n;
+  if (tid == 0) {
+    atomicAdd(&a.counters[0], 1u);
+    if ((int)blockIdx.x < tasks)  // CTAs with top-k work wait for everyone
+      while (ld_acquire(&a.counters[0]) < (unsigned)G) __nanosleep(32);
+    trace_mark(p.trace, 6);  // grid barrier passed
+  }
+  __syncthreads();
+
+  // ---------------- top-k: (sequence, node) tasks over the CTAs
+  {
+    int tseq = 0, ttile0 = 0, tm = sh_m0;
+    for (int t = blockIdx.x; t < tasks; t += G) {
+      const int sq = t / p.n, node = t - (t / p.n) * p.n;
+      while (tseq < sq) {
+        ttile0 += (tm + kBM - 1) / kBM;
+        ++tseq;
+        tm = clamp_nact(p, tseq);
       }
-      __syncthreads();
-      const int s0 = split * kBM / sp.S, s1 = (split + 1) * kBM / sp.S;
-      const int nr = s1 - s0;
-      const int total = nr * p.n;
-      for (int idx = tid; idx < total; idx += kThreads) {
-        const int c = idx / nr;
-        const int rr = s0 + (idx - c * nr);
-        if (rr < rows) {
-          float acc = 0.f;
-          for (int s = 0; s < sp.S; ++s) acc += __ldcg(&a.part[((long long)(tile * sp.S + s) * NT + c) * kBM + rr]);
-          p.logits[((long long)seq * p.n + c) * p.max_ids + row0 + rr] = acc;
-        }
-      }
-      __syncthreads();
-      if (tid == 0) {
-        unsigned old = atomicAdd(&a.done[tile], 1u);
-        if (old == (unsigned)sp.S - 1) {
-          a.arrive[tile] = 0u;
-          a.done[tile] = 0u;
-        }
-      }
+      topk_node<NT>(a, sq, node, ttile0, S, smem, tsh);
     }
   }
 
+  // ---------------- teardown: last CTA out resets the counters for the next launch
+  if (tid == 0) trace_mark(p.trace, 8);  // top-k done
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned old = atomicAdd(&a.counters[1], 1u);
+    sh_tiles = (old == (unsigned)G - 1) ? 1 : 0;
+  }
+  __syncthreads();
+  if (sh_tiles && tid == 0) {  // the last CTA: every other CTA has passed all its waits
+    a.counters[0] = 0u;
+    a.counters[1] = 0u;
+    __threadfence();
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == kLoadWarps) {
@@ -378,8 +607,27 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
   }
 }
 
+struct ScratchLayout {
+  size_t counters, part, total;
+};
+
+inline ScratchLayout scratch_layout(int batch, int max_ids, int n, int nt) {
+  const size_t max_tiles = (size_t)batch * ((max_ids + kBM - 1) / kBM);
+  const size_t units_cap = max_tiles > (size_t)kMaxSMs ? max_tiles : (size_t)kMaxSMs;
+  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  ScratchLayout L;
+  size_t off = 0;
+  L.counters = off; off += al(sizeof(unsigned) * (2 + max_tiles));
+  L.part = off;     off += al(units_cap * nt * kBM * sizeof(float));
+  L.total = off;
+  return L;
+}
+
+inline int nt_for(int n) { return n <= 16 ? 16 : n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : 256; }
+
 template <int NT>
-cudaError_t launch_nt(const HeadProblem& p, void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t stream) {
+cudaError_t launch_nt(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse, void* scratch,
+                      size_t scratch_bytes, int num_sms, cudaStream_t stream) {
   using C = Cfg<NT>;
   static bool attr = false;
   if (!attr) {
@@ -389,46 +637,54 @@ cudaError_t launch_nt(const HeadProblem& p, void* scratch, size_t scratch_bytes,
     attr = true;
   }
   const int grid = num_sms < kMaxSMs ? num_sms : kMaxSMs;
+  const ScratchLayout L = scratch_layout(p.batch, p.max_ids, p.n, NT);
+  if (L.total > scratch_bytes) return cudaErrorInvalidValue;
+  char* sc = (char*)scratch;
   TcArgs a;
   a.p = p;
-  const int max_tiles = p.batch * ((p.max_ids + kBM - 1) / kBM);
-  char* s = (char*)scratch;
-  a.arrive = (unsigned*)s;
-  a.done = (unsigned*)(s + sizeof(unsigned) * (size_t)max_tiles);
-  size_t off = (sizeof(unsigned) * 2 * (size_t)max_tiles + 255) / 256 * 256;
-  a.part = (float*)(s + off);
-  a.max_tiles = max_tiles;
-  if (off + (size_t)kMaxSMs * NT * kBM * sizeof(float) > scratch_bytes) return cudaErrorInvalidValue;
+  a.counters = (unsigned*)(sc + L.counters);
+  a.part = (float*)(sc + L.part);
+  a.topk_logit = topk_logit;
+  a.topk_id = topk_id;
+  a.lse = lse;
+  a.k = k;
+  a.max_tiles = p.batch * ((p.max_ids + kBM - 1) / kBM);
 
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = C::kSmemBytes;
   cfg.stream = stream;
-  cudaLaunchAttribute attrs[1];
+  cudaLaunchAttribute attrs[2];
   attrs[0].id = cudaLaunchAttributeCooperative;
   attrs[0].val.cooperative = 1;
+  attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attrs;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, head_tc_kernel<NT>, a);
+  cfg.numAttrs = 2;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, head_tc_kernel<NT>, a);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    cfg.numAttrs = 1;  // cooperative only
+    e = cudaLaunchKernelEx(&cfg, head_tc_kernel<NT>, a);
+  }
+  return e;
 }
 
 }  // namespace
 
 size_t head_tc_scratch_bytes(int batch, int max_ids, int n) {
-  const size_t max_tiles = (size_t)batch * ((max_ids + kBM - 1) / kBM);
-  int nt = n <= 16 ? 16 : n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : 256;
-  return (sizeof(unsigned) * 2 * max_tiles + 255) / 256 * 256 + (size_t)kMaxSMs * nt * kBM * sizeof(float);
+  return scratch_layout(batch, max_ids, n, nt_for(n)).total;
 }
 
-cudaError_t launch_head_tc(const HeadProblem& p, void* scratch, size_t scratch_bytes, int num_sms,
-                           cudaStream_t stream) {
-  if (p.d % kBK != 0 || p.n < 1 || p.n > 256 || p.ldw % 8 != 0) return cudaErrorNotSupported;
-  if (p.n <= 16) return launch_nt<16>(p, scratch, scratch_bytes, num_sms, stream);
-  if (p.n <= 32) return launch_nt<32>(p, scratch, scratch_bytes, num_sms, stream);
-  if (p.n <= 64) return launch_nt<64>(p, scratch, scratch_bytes, num_sms, stream);
-  if (p.n <= 128) return launch_nt<128>(p, scratch, scratch_bytes, num_sms, stream);
-  return launch_nt<256>(p, scratch, scratch_bytes, num_sms, stream);
+cudaError_t launch_head_tc(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse,
+                           void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t stream) {
+  if (p.d % kBK != 0 || p.n < 1 || p.n > 256 || p.ldw % 8 != 0 || k < 1 || k > kMaxK) return cudaErrorNotSupported;
+  if (p.n <= 16) return launch_nt<16>(p, k, topk_logit, topk_id, lse, scratch, scratch_bytes, num_sms, stream);
+  if (p.n <= 32) return launch_nt<32>(p, k, topk_logit, topk_id, lse, scratch, scratch_bytes, num_sms, stream);
+  if (p.n <= 64) return launch_nt<64>(p, k, topk_logit, topk_id, lse, scratch, scratch_bytes, num_sms, stream);
+  if (p.n <= 128) return launch_nt<128>(p, k, topk_logit, topk_id, lse, scratch, scratch_bytes, num_sms, stream);
+  return launch_nt<256>(p, k, topk_logit, topk_id, lse, scratch, scratch_bytes, num_sms, stream);
 }
 
 }  // namespace nanospec

@@ -28,14 +28,19 @@ struct HeadProblem {
   int max_ids;              // ids capacity per sequence (row stride of logits)
   int n_shards;             // row(g) = g / n_shards
   float* logits;            // fp32 [batch x n x max_ids]
+  unsigned long long* trace; // debug phase trace or null
 };
+
+// Debug phase-trace buffer (nanospec_debug_set_trace); null = off.
+unsigned long long* trace_buffer();
 
 // Phase 1 (a3+a4): gathered contraction into the fp32 logits staging buffer.
 cudaError_t launch_head_simt(const HeadProblem& p, int num_sms, cudaStream_t stream);
-// Tensor-core variant; returns cudaErrorNotSupported when the shape is not
-// covered (caller falls back to SIMT only if the caller asked for AUTO).
-cudaError_t launch_head_tc(const HeadProblem& p, void* scratch, size_t scratch_bytes, int num_sms,
-                           cudaStream_t stream);
+// Tensor-core variant, a3+a4+a5 fused in one kernel (writes the top-k, lse and,
+// if p.logits != null, the debug logits).  Returns cudaErrorNotSupported when
+// the shape is not covered (the caller falls back to SIMT only for AUTO).
+cudaError_t launch_head_tc(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse,
+                           void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t stream);
 size_t head_tc_scratch_bytes(int batch, int max_ids, int n);
 
 // Phase 2 (a5): per (sequence, node) top-k by (value desc, id asc) + lse.

@@ -161,11 +161,12 @@ __device__ void compact(const StateView& sv, int seq, int* sh_scan) {
   const int w0 = tid * per;
   const int w1 = min(sv.words, w0 + per);
   int c = 0;
-  for (int w = w0; w < w1; ++w) c += __popc(bm[w]);
+#pragma unroll 8
+  for (int w = w0; w < w1; ++w) c += __popc(__ldcg(bm + w));
   int n;
   int off = block_exclusive_scan(c, sh_scan, &n);
   for (int w = w0; w < w1; ++w) {
-    uint32_t b = bm[w];
+    uint32_t b = __ldcg(bm + w);
     while (b) {
       int bit = __ffs(b) - 1;
       b &= b - 1;
@@ -213,6 +214,132 @@ __global__ void __launch_bounds__(512) state_append_kernel(AppendArgs args) {
   }
 }
 
+// Per-step fast path of a2 (rule R1, no reset, both lists together <= 512
+// ids and <= W_max, W_max <= 8192): one CTA per sequence.  The sequence's
+// bitmap and the new ids are staged in shared memory; tuple(.) dedup is a
+// shared-memory hash (min position per (list, id)); window counts are updated
+// with returning atomics (all decrements, then all increments), so the bit
+// flips are known without re-reading cnt; I is recompacted into shared memory
+// and written back with coalesced stores.  Global round trips: {meta, bitmap,
+// lists} -> ring slots -> decrements -> increments.
+constexpr int kFastThreads = 512;
+constexpr int kFastMaxW = 8192;
+constexpr int kHashSlots = 2048;
+
+__global__ void __launch_bounds__(kFastThreads) state_update_fast_kernel(AppendArgs args, unsigned long long* trace) {
+  extern __shared__ uint32_t dyn[];
+  __shared__ int32_t hkey[kHashSlots];
+  __shared__ int32_t hpos[kHashSlots];
+  __shared__ int sh_scan[40];
+  __shared__ long long sh_total;
+  __shared__ int sh_err;
+  if (threadIdx.x == 0) trace_mark(trace, 9);  // state: start
+  // let the dependent head kernel get resident and run its prologue meanwhile
+  asm volatile("griddepcontrol.launch_dependents;");
+  const StateView& sv = args.sv;
+  const int seq = args.seq0 + blockIdx.x;
+  const int tid = threadIdx.x;
+  const int W = sv.w_max;
+  uint32_t* bm_s = dyn;                                  // [words]
+  int32_t* ids_s = reinterpret_cast<int32_t*>(dyn + sv.words);  // [W]
+  const int la = (int)args.a.len, lb = (int)args.b.len;
+  const int L = la + lb;
+  uint32_t* bm = sv.bitmap + (long long)seq * sv.words;
+  int32_t* ring = sv.ring + (long long)seq * W;
+  int32_t* cnt = sv.cnt + (long long)seq * sv.v_local;
+  if (tid == 0) { sh_total = sv.meta[seq].total; sh_err = 0; }
+  int32_t e = -1;
+  if (tid < la) e = args.a.ptr[(long long)(seq - args.seq0) * args.a.seq_stride + tid];
+  else if (tid < L) e = args.b.ptr[(long long)(seq - args.seq0) * args.b.seq_stride + (tid - la)];
+  {
+    uint32_t tmp[32];  // all bitmap loads of this thread in flight at once (<= 16384 words)
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int w = tid + i * kFastThreads;
+      if (w < sv.words) tmp[i] = bm[w];
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int w = tid + i * kFastThreads;
+      if (w < sv.words) bm_s[w] = tmp[i];
+    }
+  }
+  for (int h = tid; h < kHashSlots; h += kFastThreads) { hkey[h] = -1; hpos[h] = 0x7fffffff; }
+  __syncthreads();
+  if (tid == 0) trace_mark(trace, 10);  // state: bitmap + lists staged
+  // tuple(.): keep the first occurrence of every id within its own list
+  const bool valid = tid < L && e >= 0 && e < sv.vocab;
+  if (tid < L && !valid) sh_err = 1;
+  int slot_h = -1;
+  if (valid) {
+    const int32_t key = e * 2 + (tid < la ? 0 : 1);
+    int h = (int)(((uint32_t)key * 2654435761u) >> 21) & (kHashSlots - 1);
+    while (true) {
+      const int32_t old = atomicCAS(&hkey[h], -1, key);
+      if (old == -1 || old == key) break;
+      h = (h + 1) & (kHashSlots - 1);
+    }
+    atomicMin(&hpos[h], tid);
+    slot_h = h;
+  }
+  __syncthreads();
+  const bool keep = valid && hpos[slot_h] == tid;
+  int nk;
+  const int pos = block_exclusive_scan(keep ? 1 : 0, sh_scan, &nk);
+  const long long total = sh_total;
+  int slot = (int)(total % W) + pos;  // pos < W: one wrap at most
+  if (slot >= W) slot -= W;
+  int32_t old = -1;
+  if (keep && total + pos >= W) old = ring[slot];
+  // decrements for the evicted slots
+  if (tid == 0) trace_mark(trace, 11);  // state: ring slots read
+  if (old >= 0 && is_local(sv, old)) {
+    const int32_t l = local_of(sv, old);
+    if (atomicSub(&cnt[l], 1) == 1) atomicAnd(&bm_s[l >> 5], ~(1u << (l & 31)));
+  }
+  __syncthreads();
+  // increments for the appended ids
+  if (tid == 0) trace_mark(trace, 12);  // state: decrements done
+  if (keep) {
+    ring[slot] = e;
+    if (is_local(sv, e)) {
+      const int32_t l = local_of(sv, e);
+      if (atomicAdd(&cnt[l], 1) == 0) atomicOr(&bm_s[l >> 5], 1u << (l & 31));
+    }
+  }
+  __syncthreads();
+  if (tid == 0) trace_mark(trace, 13);  // state: increments done
+  // write the bitmap back; recompact I (ascending) into shared memory
+  for (int w = tid; w < sv.words; w += kFastThreads) bm[w] = bm_s[w];
+  const int per = (sv.words + kFastThreads - 1) / kFastThreads;
+  const int w0 = tid * per, w1 = min(sv.words, w0 + per);
+  int c = 0;
+  for (int w = w0; w < w1; ++w) c += __popc(bm_s[w]);
+  int n;
+  int off = block_exclusive_scan(c, sh_scan, &n);
+  if (tid == 0) trace_mark(trace, 15);  // state: bitmap written back, counts scanned
+  for (int w = w0; w < w1; ++w) {
+    uint32_t b = bm_s[w];
+    while (b) {
+      const int bit = __ffs(b) - 1;
+      b &= b - 1;
+      const int32_t l = (w << 5) + bit;
+      if (off < W) ids_s[off] = sv.n_shards <= 1 ? l : l * sv.n_shards + sv.rank;
+      ++off;
+    }
+  }
+  __syncthreads();
+  int32_t* ids = sv.ids + (long long)seq * W;
+  const int nn = min(n, W);
+  for (int j = tid; j < nn; j += kFastThreads) ids[j] = ids_s[j];  // coalesced
+  if (tid == 0) {
+    sv.meta[seq].total = total + nk;
+    sv.meta[seq].n_active = n;
+    if (sh_err) sv.meta[seq].err |= 1;
+    trace_mark(trace, 14);  // state: done
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_state_append(const StateView& sv, int seq0, int nseq, int reset,
@@ -225,6 +352,22 @@ cudaError_t launch_state_append(const StateView& sv, int seq0, int nseq, int res
   args.reset = reset;
   args.a = ListArg{a, a_len, a_stride, a_dedup};
   args.b = ListArg{b, b_len, b_stride, b_dedup};
+  const long long L = (a ? a_len : 0) + (b ? b_len : 0);
+  if (!reset && sv.rule == 0 && a_dedup && b_dedup && L <= kFastThreads && L <= sv.w_max &&
+      sv.words <= 16384 && sv.w_max <= kFastMaxW) {
+    if (!a) args.a.len = 0;
+    if (!b) args.b.len = 0;
+    const size_t smem = sizeof(uint32_t) * ((size_t)sv.words + (size_t)sv.w_max);
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(state_update_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (16384 + kFastMaxW) * (int)sizeof(uint32_t));
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    state_update_fast_kernel<<<nseq, kFastThreads, smem, stream>>>(args, trace_buffer());
+    return cudaGetLastError();
+  }
   state_append_kernel<<<nseq, 512, 0, stream>>>(args);
   return cudaGetLastError();
 }

@@ -1,0 +1,105 @@
+"""Phase timeline of one fused head call (debug trace, globaltimer ns per CTA).
+
+    python scripts/trace_head.py [--n 60] [--m 3072] [--cold]
+"""
+import argparse
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2605_26444_b200 as P  # noqa: E402
+from paper_2605_26444_b200 import _native as N  # noqa: E402
+from synthetic import inputs as SI  # noqa: E402
+
+EVENTS = ["start", "dep_ok", "rowptr", "loads_landed", "mma_done", "epilogue", "grid_bar", "tk_loaded",
+          "topk_done", "tk_thresh", "tk_counted", "tk_compacted", "tk_ranked"]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=60)
+    ap.add_argument("--m", type=int, default=3072)
+    ap.add_argument("--k", type=int, default=10)
+    ap.add_argument("--reps", type=int, default=5)
+    args = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    V, d = 128256, 4096
+    W = SI.bf16_weights(V, d, seed=0, device=dev)
+    ids = np.random.default_rng(0).choice(V, args.m, replace=False).astype(np.int32)
+    st = P.ActiveVocab(V, 3072 if args.m <= 3072 else args.m, device=dev)
+    st.init(0, torch.as_tensor(ids, device=dev))
+    H = SI.bf16_hidden(args.n, d, seed=1, device=dev).reshape(1, args.n, d)
+    out = P.HeadOutputs(1, args.n, args.k, st.w_max, dev)
+    trace = torch.zeros(256 * 16 + 512, dtype=torch.int64, device=dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(3):
+        P.draft_logits_topk(st, W, H, args.k, impl="tc", out=out)
+    torch.cuda.synchronize()
+    for mode in ("cold", "warm"):
+        rows = []
+        for r in range(args.reps):
+            if mode == "cold":
+                flush.fill_(r & 0xff)
+            torch.cuda.synchronize()
+            trace.zero_()
+            N.check(N.lib().nanospec_debug_set_trace(trace.data_ptr(), 256), "set_trace")
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            P.draft_logits_topk(st, W, H, args.k, impl="tc", out=out)
+            e1.record()
+            torch.cuda.synchronize()
+            N.check(N.lib().nanospec_debug_set_trace(None, 0), "set_trace")
+            full = trace.cpu().numpy().astype(np.int64)
+            clk = full[256 * 16:].reshape(256, 2)
+            t = full[:256 * 16].reshape(256, 16)
+            ctas = int((t[:, 0] > 0).sum())
+            t = t[:ctas]
+            t0 = t[:, 0].min()
+            rows.append((e0.elapsed_time(e1) * 1e3, t, t0))
+        print(f"=== {mode} (m={args.m}, n={args.n}); event-timed call: "
+              f"{np.median([r[0] for r in rows]):.2f} us median of {args.reps}")
+        ev_us, t, t0 = rows[-1]
+
+        for e, name in enumerate(EVENTS):
+            col = t[:, e]
+            col = col[col > 0]
+            if len(col) == 0:
+                continue
+            rel = (col - t0) / 1e3
+            print(f"  {name:13s} n={len(col):3d}  min {rel.min():7.2f}  med {np.median(rel):7.2f}  max {rel.max():7.2f} us")
+
+
+def trace_state():
+    dev = torch.device("cuda", 0)
+    V = 128256
+    pools = SI.disjoint_pools(V, 3072 + 126, 1)
+    prompt, ups = SI.cyclic_fresh_updates(pools[0], 3072, 8)
+    st = P.ActiveVocab(V, 3072, device=dev)
+    st.init(0, torch.as_tensor(prompt, device=dev))
+    trace = torch.zeros(256 * 16, dtype=torch.int64, device=dev)
+    names = ["start", "staged", "ring_read", "decrements", "increments", "done", "scanned"]
+    for i, (d, v) in enumerate(ups):
+        dd, vv = torch.as_tensor(d, device=dev), torch.as_tensor(v, device=dev)
+        torch.cuda.synchronize()
+        N.check(N.lib().nanospec_debug_set_trace(trace.data_ptr(), 256), "set_trace")
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        st.update(0, dd, vv)
+        e1.record()
+        torch.cuda.synchronize()
+        N.check(N.lib().nanospec_debug_set_trace(None, 0), "set_trace")
+        t = trace.view(256, 16)[0].cpu().numpy().astype(np.int64)
+        rel = [(t[9 + j] - t[9]) / 1e3 for j in range(7)]
+        print(f"state update {i}: event {e0.elapsed_time(e1) * 1e3:.2f} us; " +
+              " ".join(f"{n}={r:.2f}" for n, r in zip(names, rel)))
+
+
+if __name__ == "__main__":
+    if "--state" in sys.argv:
+        sys.argv.remove("--state")
+        trace_state()
+    main()
