@@ -38,6 +38,10 @@ CONFIGS = {
     "llama": dict(model="llama-3.1-8b", vocab=128256, d=4096, w_max=3072),
     "qwen": dict(model="qwen-2.5-7b", vocab=152064, d=3584, w_max=3072),
     "tiny": dict(model="tiny", vocab=1000, d=64, w_max=256),
+    # BASELINE.json configs[3]: 64 independent sequences, data-parallel over the ranks
+    "dp64": dict(model="llama-3.1-8b", vocab=128256, d=4096, w_max=3072, batch=64),
+    # BASELINE.json configs[4]: 32k-token Zipf window (~11k active), vocab-parallel over the ranks
+    "vp32k": dict(model="llama-3.1-8b", vocab=128256, d=4096, w_max=32768),
 }
 
 
@@ -369,6 +373,11 @@ def run_ours(args):
 
     # roofline of the dominant kernel (the head call; algorithmic bytes SURVEY 8(d))
     peak, peak_src = load_peaks()
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath) and args.config == "llama" and n == 60 and k == 10:
+        with open(tpath) as f:
+            traffic = json.load(f).get("traffic_bytes")
     alg_bytes = Wm * d * 2 + n * d * 2 + Wm * 4 + n * k * 8 + n * 4
     achieved = alg_bytes / (us_head * 1e-6) / 1e9
 
@@ -392,7 +401,7 @@ def run_ours(args):
         "breakdown": {"us_step": round(us_step, 3), "us_head_call": round(us_head, 3),
                       "us_state_update": round(us_upd, 3), "head_gbps": round(achieved, 1)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
+                     "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                      "kernel": "draft_logits_topk call (contraction + top-k select)",
                      "alg_bytes_per_launch": alg_bytes},
         "dense": {kk: (round(vv, 3) if isinstance(vv, float) else vv) for kk, vv in dense.items()},
@@ -417,10 +426,179 @@ def _mm_out_dtype_ok(torch):
         return False
 
 
+def _timed_graph(torch, fn, count, stream):
+    """Capture `count` calls of fn(i) in one CUDA graph, replay once, return us per call."""
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for i in range(count):
+            fn(i)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    g.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e3 / count
+
+
+def run_dp64(args):
+    """configs[3]: 64 independent Llama-shape sequences (|I| = 3072 exact each),
+    split over the ranks (64 / N per rank, one batched update + one batched head
+    call per step; no collective on the path).  value = us per batched step over
+    all 64 sequences (max over ranks), i.e. the wall time of one data-parallel
+    decode step of the whole batch."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_26444_b200 as P
+    from paper_2605_26444_b200 import parallel as PAR
+    from synthetic import inputs as SI
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS["dp64"]
+    V, d, Wm, B = cfg["vocab"], cfg["d"], cfg["w_max"], cfg["batch"]
+    n, k = args.n_nodes, args.k
+    mine = list(PAR.dp_sequences(B, rank, world))
+    b = len(mine)
+    W = SI.bf16_weights(V, d, seed=0, device=dev)
+    pool = Wm + 128
+    pools = SI.disjoint_pools(V, pool, 40, seed=3)  # 40 disjoint pools; sequence s uses pool s % 40
+    st = P.ActiveVocab(V, Wm, batch=b, device=dev)
+    steps_needed = args.warmup + args.steps + 2
+    ud, uv = [], []
+    for i, sq in enumerate(mine):
+        prompt, ups = SI.cyclic_fresh_updates(np.roll(pools[sq % 40], 7 * sq), Wm, steps_needed)
+        st.init(i, torch.as_tensor(prompt, device=dev))
+        ud.append(np.stack([u[0] for u in ups]))
+        uv.append(np.stack([u[1] for u in ups]))
+    ud = torch.as_tensor(np.stack(ud, 1), device=dev)  # [steps, b, 60]
+    uv = torch.as_tensor(np.stack(uv, 1), device=dev)
+    H = SI.bf16_hidden(n, d, seed=1 + rank, device=dev, batch=b)
+    out = P.HeadOutputs(b, n, k, Wm, dev)
+    torch.cuda.synchronize()
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+
+    def step(i):
+        st.update_batch(ud[i], uv[i])
+        P.draft_logits_topk(st, W, H, k, impl=args.head, out=out)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    us = _timed_graph(torch, lambda i: step(args.warmup + i), args.steps, stream)
+    if world > 1:
+        t = torch.tensor([us], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        us = float(t.item())
+    peak, peak_src = load_peaks()
+    alg = b * (Wm * d * 2 + n * d * 2 + Wm * 4 + n * k * 8 + n * 4)
+    gbps = alg / (us * 1e-6) / 1e9
+    line = {"metric": METRIC, "value": round(us, 3), "unit": "us/step (64 sequences)", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": us / 1e3, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"dp64: 64 x llama-3.1-8b draft heads, |I|={Wm} each, n={n} k={k}",
+                       "parallelism": f"dp{world} ({b} sequences per rank)", "head": args.head},
+            "roofline": {"bound": "hbm", "achieved": round(gbps, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(gbps / peak, 4), "traffic": None, "peak_source": peak_src,
+                         "kernel": "update_batch + batched draft_logits_topk, per rank"},
+            "gpu_launches": 2 * args.steps}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_vp32k(args):
+    """configs[4]: a 32k-token Zipf window (~11k active ids) with the LM head
+    sharded over the ranks by vocabulary (rank r owns ids g % N == r); every
+    rank applies the same update lists to its state shard, runs the head on its
+    rows, and the per-shard top-k + lse meet in one NCCL all-gather followed by
+    the exact merge.  value = us per step (max over ranks)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_26444_b200 as P
+    from paper_2605_26444_b200 import parallel as PAR
+    from synthetic import inputs as SI
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS["vp32k"]
+    V, d, Wm = cfg["vocab"], cfg["d"], cfg["w_max"]
+    n, k = args.n_nodes, args.k
+    Wfull = SI.bf16_weights(V, d, seed=0, device=dev)
+    Wl = PAR.shard_rows_cyclic(Wfull, rank, world) if world > 1 else Wfull
+    del Wfull
+    z = SI.Zipf(V)
+    prompt, _ = SI.prompt_and_prefill(z, 1, Wm, 0)
+    steps = SI.decode_steps(z, 7, args.warmup + args.steps + 2)
+    st = P.ActiveVocab(V, Wm, shard_rank=rank if world > 1 else 0, n_shards=world, device=dev)
+    st.init(0, torch.as_tensor(prompt, device=dev))
+    ud = torch.as_tensor(np.stack([s_[0] for s_ in steps]), device=dev)
+    uv = torch.as_tensor(np.stack([s_[1] for s_ in steps]), device=dev)
+    H = SI.bf16_hidden(n, d, seed=1, device=dev).reshape(1, n, d)
+    out = P.HeadOutputs(1, n, k, Wm, dev)
+    torch.cuda.synchronize()
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+
+    def step(i):
+        st.update(0, ud[i], uv[i])
+        if world > 1:
+            PAR.vp_draft_logits_topk(st, Wl, H, k, impl=args.head, out=out)
+        else:
+            P.draft_logits_topk(st, Wl, H, k, impl=args.head, out=out)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    n_act = st.read(0)["n_active"]
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        step(args.warmup + i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / args.steps
+    if world > 1:
+        t = torch.tensor([us], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        us = float(t.item())
+    line = {"metric": METRIC, "value": round(us, 3), "unit": "us/step", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": us / 1e3, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"vp32k: llama-3.1-8b head, W_max={Wm} Zipf window, n={n} k={k}",
+                       "active_ids_rank0": n_act, "parallelism": f"vp{world} (cyclic vocab shards, NCCL all-gather "
+                                                               f"of per-shard top-k + lse, exact merge)",
+                       "timing": "eager launches (the all-gather is not graph-captured)", "head": args.head}}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "dp64":
+        run_dp64(args)
+    elif args.config == "vp32k":
+        run_vp32k(args)
     else:
         run_ours(args)
 

@@ -85,7 +85,10 @@ const char* nanospec_status_str(nanospec_status s);
  * `vocab` and window `w_max` (D1-D4 of SURVEY 2.2).  Per sequence it holds:
  *   bitmap  uint32[ceil(V_local/32)]  membership of I (the paper's `token_ids`,
  *                                     16,032 B at V = 128256, T6 P:449, Q14)
- *   ids     int32[w_max]              I in ascending global id (Q4), first n_active valid
+ *   ids     int32[w_max]              I as a slot table (first n_active valid): stable slots,
+ *                                     an id keeps its slot while it stays in I; the general
+ *                                     path (init) lays it out ascending (Q4)
+ *   pos     int32[V_local]            R1 only: slot of every active id
  *   ring    int32[w_max]              the last w_max stream slots (R1) / queue (R2)
  *   cnt     int32[V_local]            R1 only: occurrences of each id in the window
  *   first   int32[vocab]              dedup scratch for tuple(.) (Eq. 3/4)
@@ -133,8 +136,8 @@ nanospec_status nanospec_state_update_batch(nanospec_state st, const int32_t* d_
                                             const int32_t* d_verify_topk, int32_t k_ver, cudaStream_t stream);
 
 /* SYNCHRONISES `stream`; for tests and debugging.  Copies sequence `seq`'s
- * state to host buffers (any may be NULL): h_ids int32[w_max] (first *h_n_active
- * valid), h_bitmap uint32[ceil(V_local/32)], h_ring int32[w_max] (-1 = never
+ * state to host buffers (any may be NULL): h_ids int32[w_max] (the slot table,
+ * first *h_n_active valid; sort it for the canonical ascending order), h_bitmap uint32[ceil(V_local/32)], h_ring int32[w_max] (-1 = never
  * written), h_total = |S| (R1) or pushes (R2), h_err = the device flag. */
 nanospec_status nanospec_state_read(const nanospec_state st, int32_t seq, int32_t* h_ids, int32_t* h_n_active,
                                     uint32_t* h_bitmap, int32_t* h_ring, int64_t* h_total, int32_t* h_err,

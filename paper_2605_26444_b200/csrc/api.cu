@@ -3,6 +3,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <new>
 
 #include "nanospec.h"
@@ -28,7 +29,7 @@ constexpr size_t kAlign = 256;
 inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Layout {
-  size_t meta, bitmap, ids, ring, cnt, first, total;
+  size_t meta, bitmap, ids, ring, cnt, pos, first, total;
 };
 
 bool geometry(int32_t vocab, int32_t w_max, int32_t batch, int rule, int32_t rank, int32_t n_shards,
@@ -50,6 +51,7 @@ Layout layout(int32_t vocab, int32_t w_max, int32_t batch, int rule, int32_t v_l
   L.ids = off;    off += align_up(sizeof(int32_t) * (size_t)w_max * batch);
   L.ring = off;   off += align_up(sizeof(int32_t) * (size_t)w_max * batch);
   L.cnt = off;    off += rule == NANOSPEC_RULE_WINDOW ? align_up(sizeof(int32_t) * (size_t)v_local * batch) : 0;
+  L.pos = off;    off += rule == NANOSPEC_RULE_WINDOW ? align_up(sizeof(int32_t) * (size_t)v_local * batch) : 0;
   L.first = off;  off += align_up(sizeof(int32_t) * (size_t)vocab * batch);
   L.total = off;
   return L;
@@ -147,11 +149,12 @@ nanospec_status nanospec_state_create(nanospec_state* out, int32_t vocab, int32_
   sv.ids = (int32_t*)(base + L.ids);
   sv.ring = (int32_t*)(base + L.ring);
   sv.cnt = rule == NANOSPEC_RULE_WINDOW ? (int32_t*)(base + L.cnt) : nullptr;
+  sv.pos = rule == NANOSPEC_RULE_WINDOW ? (int32_t*)(base + L.pos) : nullptr;
   sv.first = (int32_t*)(base + L.first);
   st->ws = d_workspace;
   st->ws_bytes = ws_bytes;
   cudaError_t e = cudaSuccess;
-  // meta, bitmap, ids, cnt -> 0; ring -> -1 (0xff bytes); first -> 0x7f7f7f7f
+  // meta, bitmap, ids, cnt, pos -> 0; ring -> -1 (0xff bytes); first -> 0x7f7f7f7f
   if (e == cudaSuccess) e = cudaMemsetAsync(base + L.meta, 0, L.ring - L.meta, stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(base + L.ring, 0xff, (L.cnt ? L.cnt : L.first) - L.ring, stream);
   if (e == cudaSuccess && rule == NANOSPEC_RULE_WINDOW) e = cudaMemsetAsync(base + L.cnt, 0, L.first - L.cnt, stream);

@@ -26,6 +26,7 @@ struct StateView {
   int32_t* ids;       // [batch][w_max]
   int32_t* ring;      // [batch][w_max]
   int32_t* cnt;       // [batch][v_local]   (R1 only)
+  int32_t* pos;       // [batch][v_local]   (R1 only) slot of each active local id in ids[]
   int32_t* first;     // [batch][vocab]
 };
 

@@ -54,7 +54,8 @@ constexpr int kMaxK = 32;
 struct TcArgs {
   HeadProblem p;
   float* part;                 // [units][NT][128] fp32 partial tiles (split-K)
-  unsigned* counters;          // [0] grid arrive, [1] grid done (zero between launches)
+  float* zl;                   // [batch][n][max_ids] reduced logits (the debug output when requested)
+  unsigned* counters;          // [0] grid arrive, [1] grid done, [2 + tile] tile arrivals (zero between launches)
   float* topk_logit;           // [batch][n][k]
   int32_t* topk_id;
   float* lse;                  // [batch][n] or null
@@ -152,7 +153,9 @@ struct Cfg {
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStages = (kSmemBudget / kStageBytes) > 8 ? 8 : (kSmemBudget / kStageBytes);
   static constexpr int kTmemCols = NT < 32 ? 32 : NT;
-  static constexpr int kStageArea = kStages * kStageBytes;
+  static constexpr int kPipeArea = kStages * kStageBytes;
+  static constexpr int kTopkArea = 2 * kCandCap * 4;  // top-k phase staging
+  static constexpr int kStageArea = kPipeArea > kTopkArea ? kPipeArea : kTopkArea;
   static constexpr int kSmemBytes = kStageArea + 1024 /*align*/ + 256 /*barriers*/;
   static_assert(2 * kStages + 3 <= 30, "barrier area");
   static constexpr int kHChunks = NT * 8;                 // 16-B chunks of one H stage
@@ -160,11 +163,11 @@ struct Cfg {
 };
 
 struct TopkSmem {
-  float wthr[kWarps];
-  float wmax[kWarps];
+  float wmax[kWarps];     // per-warp max, sum exp(v - max), threshold candidate
   float wsum[kWarps];
-  int wcnt[kWarps];
-  int woff[kWarps + 1];
+  float wthr[kWarps];
+  float T;                // candidate threshold of the chunk
+  int ncand;
   int nbest;
   float best_v[kMaxK];
   int32_t best_g[kMaxK];
@@ -175,156 +178,176 @@ __device__ __forceinline__ bool ranks_before(float va, int32_t ga, float vb, int
   return ka > kb || (ka == kb && ga < gb);
 }
 
-// Top-k + lse of one (sequence, node), the whole CTA.  Logits are the sums of
-// the S split partials (fixed split order) of every active row, gathered with
-// all loads of a thread in flight at once, staged (value, id) in shared memory;
-// then T = max over warps of the k-th largest lane maximum (a lower bound on
-// the k-th largest value), the values >= T are compacted and ranked by
-// counting against each other (value desc, id asc).
+// k-th largest (k <= 32) of one float per lane, by counting (ties by lane).
+__device__ __forceinline__ float warp_kth_largest(float x, int k) {
+  const int lane = threadIdx.x & 31;
+  int rank = 0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float o = __shfl_sync(0xffffffffu, x, j);
+    rank += (o > x || (o == x && j < lane)) ? 1 : 0;
+  }
+  const unsigned sel = __ballot_sync(0xffffffffu, rank == k - 1);
+  return __shfl_sync(0xffffffffu, x, __ffs(sel) - 1);
+}
+
+// Top-k + lse of one (sequence, node), the whole CTA; every phase runs on all
+// warps in parallel (a single warp executes ~6 cycles per instruction here):
+//  1. each thread cp.async's its rows' S split partials and ids (<= 2 float4
+//     groups per chunk) into its own shared-memory slots -- all in flight at
+//     once, no registers held -- then sums them in split order (fixed order:
+//     equal rows give bit-equal logits) and keeps (max, sum exp) online;
+//  2. per-warp (max, sum exp) and, for k > 16, the k-th largest lane maximum;
+//  3. warp 0 combines the 17 warp summaries: lse partial and a threshold T that
+//     at least k values reach (k <= 16: the k-th largest warp maximum; else the
+//     largest per-warp k-th lane maximum);
+//  4. values >= T (plus the running best) are compacted into shared memory and
+//     ranked by counting (value desc, id asc).
 template <int NT>
-__device__ void topk_node(const TcArgs& a, int seq, int node, int tile_base, int S, uint8_t* smem, TopkSmem& sh) {
-  using C = Cfg<NT>;
+__device__ void topk_node(const TcArgs& a, int seq, int node, int m, uint8_t* smem, TopkSmem& sh) {
   const HeadProblem& p = a.p;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int m = clamp_nact(p, seq);
   const int k = a.k;
   const int32_t* ids = p.ids_base + (long long)seq * p.ids_stride;
   const long long ob = ((long long)seq * p.n + node) * k;
-  // shared memory: [vals cap][gids cap][cand_v kCandCap][cand_g kCandCap]
-  constexpr int kCap = ((C::kStageArea - 2 * kCandCap * 4) / 8) & ~127;
-  float* vals = reinterpret_cast<float*>(smem);
-  int32_t* gids = reinterpret_cast<int32_t*>(smem + (size_t)kCap * 4);
-  float* cv = reinterpret_cast<float*>(smem + (size_t)kCap * 8);
-  int32_t* cg = reinterpret_cast<int32_t*>(smem + (size_t)kCap * 8 + kCandCap * 4);
+  float* cv = reinterpret_cast<float*>(smem);
+  int32_t* cg = reinterpret_cast<int32_t*>(cv + kCandCap);
+  constexpr int kChunk = 2 * kThreads * 4;  // rows per chunk
   if (tid == 0) sh.nbest = 0;
-  float run_max = -INFINITY, run_sum = 0.f;  // online lse over chunks (block-uniform)
-  for (int c0 = 0; c0 < m; c0 += kCap) {
-    const int mc = min(kCap, m - c0);
-    const int ng = (mc + 3) / 4;  // float4 row groups (never straddle a 128-row tile)
-    __syncthreads();              // previous chunk's readers are done
-    // 1. gather + sum: thread t takes groups t, t + kThreads, ... two at a time
-    float lmax = -INFINITY;
-    for (int g0 = tid; g0 < ng; g0 += 2 * kThreads) {
-      float4 acc[2];
+  float run_max = -INFINITY, run_sum = 0.f;  // online lse over chunks (kept by warp 0 lane 0)
+  for (int c0 = 0; c0 < m; c0 += kChunk) {
+    const int mc = min(kChunk, m - c0);
+    // ---- 1. gather the reduced logits and ids (<= 2 float4 groups per thread, all in flight)
+    float v[8];
+    int32_t g[8];
+    float tm = -INFINITY;
+    {
+      const float* zrow = a.zl + ((long long)seq * p.n + node) * p.max_ids;
+      float4 x[2];
       int4 gi[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        acc[h] = make_float4(0.f, 0.f, 0.f, 0.f);
-        const int g = g0 + h * kThreads;
-        if (g < ng) {
-          const int j = c0 + 4 * g;  // first row of the group
-          const float* src = a.part + ((long long)(tile_base + j / kBM) * S * NT + node) * kBM + (j % kBM);
-          for (int s0 = 0; s0 < S; s0 += 8) {
-            float4 x[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-              if (s0 + q < S) x[q] = __ldcg(reinterpret_cast<const float4*>(src + (long long)(s0 + q) * NT * kBM));
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-              if (s0 + q < S) { acc[h].x += x[q].x; acc[h].y += x[q].y; acc[h].z += x[q].z; acc[h].w += x[q].w; }
-          }
-          if (((p.ids_stride | j) & 3) == 0 && j + 3 < m) {
-            gi[h] = __ldg(reinterpret_cast<const int4*>(ids + j));
+        const int jj = 4 * (tid + h * kThreads);
+        const int j = c0 + jj;
+        x[h] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        gi[h] = make_int4(0, 0, 0, 0);
+        if (jj < mc) {
+          if (((((uintptr_t)(zrow + j)) | ((uintptr_t)(ids + j))) & 15) == 0 && j + 3 < m) {
+            x[h] = __ldcg(reinterpret_cast<const float4*>(zrow + j));
+            gi[h] = __ldcg(reinterpret_cast<const int4*>(ids + j));
           } else {
-            gi[h].x = ids[min(j, m - 1)];
-            gi[h].y = ids[min(j + 1, m - 1)];
-            gi[h].z = ids[min(j + 2, m - 1)];
-            gi[h].w = ids[min(j + 3, m - 1)];
+            x[h].x = __ldcg(zrow + j);
+            gi[h].x = __ldg(ids + j);
+            if (j + 1 < m) { x[h].y = __ldcg(zrow + j + 1); gi[h].y = __ldg(ids + j + 1); }
+            if (j + 2 < m) { x[h].z = __ldcg(zrow + j + 2); gi[h].z = __ldg(ids + j + 2); }
+            if (j + 3 < m) { x[h].w = __ldcg(zrow + j + 3); gi[h].w = __ldg(ids + j + 3); }
           }
         }
       }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int g = g0 + h * kThreads;
-        if (g < ng) {
-          const int jj = 4 * g;
-          const float v[4] = {acc[h].x, acc[h].y, acc[h].z, acc[h].w};
-          const int32_t gg[4] = {gi[h].x, gi[h].y, gi[h].z, gi[h].w};
+        const int jj = 4 * (tid + h * kThreads);
+        const float vv[4] = {x[h].x, x[h].y, x[h].z, x[h].w};
+        const int32_t gg[4] = {gi[h].x, gi[h].y, gi[h].z, gi[h].w};
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            if (jj + i < mc) {
-              vals[jj + i] = v[i];
-              gids[jj + i] = gg[i];
-              lmax = fmaxf(lmax, v[i]);
-              if (p.logits) p.logits[((long long)seq * p.n + node) * p.max_ids + c0 + jj + i] = v[i];
-            }
-          }
+        for (int i = 0; i < 4; ++i) {
+          const bool ok = jj + i < mc;
+          v[4 * h + i] = ok ? vv[i] : -INFINITY;
+          g[4 * h + i] = gg[i];
+          if (ok) tm = fmaxf(tm, vv[i]);
         }
       }
     }
-    if (tid == 0 && c0 == 0) trace_mark(p.trace, 7);  // logits gathered
-    // 2. per-warp k-th largest lane maximum (rank by counting over the 32 lanes)
+    float ts = 0.f;
+    if (tm != -INFINITY) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) ts += __expf(v[i] - tm);  // exp(-inf) = 0 for padding
+    }
+    if (tid == 0 && c0 == 0) trace_mark(p.trace, 7);  // gathered
+    // ---- 2. per-warp summaries
+    float wm = tm;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+    float ws = (tm == -INFINITY) ? 0.f : ts * __expf(tm - wm);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ws += __shfl_xor_sync(0xffffffffu, ws, o);
+    const float wt = k > 16 ? warp_kth_largest(tm, k) : -INFINITY;
+    if (lane == 0) { sh.wmax[warp] = wm; sh.wsum[warp] = ws; sh.wthr[warp] = wt; }
+    if (tid == 0) sh.ncand = sh.nbest;  // the running best go first
+    __syncthreads();
+    // ---- 3. every warp combines the 17 warp summaries itself (no extra
+    //         barrier): lse partial (kept by thread 0) and the threshold T
+    float T;
     {
-      int rank = 0;
+      const float x = lane < kWarps ? sh.wmax[lane] : -INFINITY;
+      float M = x;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float o = __shfl_sync(0xffffffffu, lmax, j);
-        rank += (o > lmax || (o == lmax && j < lane)) ? 1 : 0;
+      for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+      if (warp == 0) {
+        float es = (lane < kWarps && x != -INFINITY) ? sh.wsum[lane] * __expf(x - M) : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
+        if (lane == 0 && M != -INFINITY) {
+          const float nm = fmaxf(run_max, M);
+          run_sum = (run_max == -INFINITY ? 0.f : run_sum * __expf(run_max - nm)) + es * __expf(M - nm);
+          run_max = nm;
+        }
       }
-      const unsigned sel = __ballot_sync(0xffffffffu, rank == min(k, 32) - 1);
-      const float kth = __shfl_sync(0xffffffffu, lmax, __ffs(sel) - 1);
-      float wm = lmax;
+      if (k <= 16) {
+        // k-th largest warp maximum, by counting over the kWarps lanes
+        int rank = 0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
-      if (lane == 0) { sh.wthr[warp] = kth; sh.wmax[warp] = wm; }
+        for (int j = 0; j < kWarps; ++j) {
+          const float o = __shfl_sync(0xffffffffu, x, j);
+          rank += (o > x || (o == x && j < lane)) ? 1 : 0;
+        }
+        const unsigned sel = __ballot_sync(0xffffffffu, lane < kWarps && rank == k - 1);
+        T = __shfl_sync(0xffffffffu, x, __ffs(sel) - 1);
+      } else {
+        T = lane < kWarps ? sh.wthr[lane] : -INFINITY;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) T = fmaxf(T, __shfl_xor_sync(0xffffffffu, T, o));
+      }
+      if (sh.nbest == k) T = fmaxf(T, sh.best_v[k - 1]);
     }
-    __syncthreads();
-    float T = -INFINITY, cmax = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) { T = fmaxf(T, sh.wthr[w]); cmax = fmaxf(cmax, sh.wmax[w]); }
-    const int nprev = sh.nbest;
-    if (nprev == k) T = fmaxf(T, sh.best_v[k - 1]);
     if (tid == 0 && c0 == 0) trace_mark(p.trace, 9);  // threshold
-    // 3. count candidates >= T per warp (same element order as the compaction
-    //    below) and the chunk's sum exp(v - cmax)
-    int wc = 0;
-    float es = 0.f;
-    for (int base = warp * 32; base < mc; base += kThreads) {
-      const int jj = base + lane;
-      const float v = jj < mc ? vals[jj] : -INFINITY;
-      wc += __popc(__ballot_sync(0xffffffffu, jj < mc && v >= T));
-      if (jj < mc) es += __expf(v - cmax);
+    // ---- 4. compact the values >= T (plus the running best), then rank
+    const int nprev = sh.nbest;
+    if (tid < nprev) { cv[tid] = sh.best_v[tid]; cg[tid] = sh.best_g[tid]; }
+    int cnt = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) cnt += (v[i] != -INFINITY && v[i] >= T) ? 1 : 0;
+    if (cnt) {
+      int slot = atomicAdd(&sh.ncand, cnt);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (v[i] != -INFINITY && v[i] >= T) {
+          if (slot < kCandCap) { cv[slot] = v[i]; cg[slot] = g[i]; }
+          ++slot;
+        }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
-    if (lane == 0) { sh.wcnt[warp] = wc; sh.wsum[warp] = es; }
     __syncthreads();
-    if (warp == 0) {
-      const int c = lane < kWarps ? sh.wcnt[lane] : 0;
-      int x = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-      }
-      if (lane < kWarps) sh.woff[lane] = nprev + x - c;
-      if (lane == 31) sh.woff[kWarps] = nprev + x;
-    }
-    float csum = 0.f;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) csum += sh.wsum[w];
-    const float nm = fmaxf(run_max, cmax);
-    run_sum = (run_max == -INFINITY ? 0.f : run_sum * __expf(run_max - nm)) + csum * __expf(cmax - nm);
-    run_max = nm;
-    __syncthreads();
-    if (sh.woff[kWarps] > kCandCap) {
-      // Degenerate ties (e.g. h = 0): more than kCandCap values >= T.  Exact
-      // but slow: one thread walks the chunk in row order (= ascending id)
-      // keeping a sorted best-k list; ties keep the earlier (smaller) id.
+    if (tid == 0 && c0 == 0) trace_mark(p.trace, 10);  // compacted
+    const int tot = sh.ncand;
+    if (tid == 0 && c0 == 0 && p.trace) p.trace[(long long)blockIdx.x * kTraceSlots + 15] = tot;
+    if (tot > kCandCap) {
+      // Degenerate ties (e.g. h = 0): exact but slow fallback -- one thread
+      // re-walks the chunk in row order (= ascending id) with a sorted best-k.
       if (tid == 0) {
         int nb = sh.nbest;
         for (int jj = 0; jj < mc; ++jj) {
-          const float v = vals[jj];
-          const int32_t g = gids[jj];
-          if (nb == k && !ranks_before(v, g, sh.best_v[k - 1], sh.best_g[k - 1])) continue;
+          const int j = c0 + jj;
+          const float vv = __ldcg(a.zl + ((long long)seq * p.n + node) * p.max_ids + j);
+          const int32_t gg = __ldg(ids + j);
+          if (nb == k && !ranks_before(vv, gg, sh.best_v[k - 1], sh.best_g[k - 1])) continue;
           int pos = nb < k ? nb : k - 1;
-          while (pos > 0 && ranks_before(v, g, sh.best_v[pos - 1], sh.best_g[pos - 1])) {
+          while (pos > 0 && ranks_before(vv, gg, sh.best_v[pos - 1], sh.best_g[pos - 1])) {
             sh.best_v[pos] = sh.best_v[pos - 1];
             sh.best_g[pos] = sh.best_g[pos - 1];
             --pos;
           }
-          sh.best_v[pos] = v;
-          sh.best_g[pos] = g;
+          sh.best_v[pos] = vv;
+          sh.best_g[pos] = gg;
           if (nb < k) ++nb;
         }
         sh.nbest = nb;
@@ -332,24 +355,6 @@ __device__ void topk_node(const TcArgs& a, int seq, int node, int tile_base, int
       __syncthreads();
       continue;
     }
-    const int tot = sh.woff[kWarps];
-    if (tid == 0 && c0 == 0) trace_mark(p.trace, 10);  // counted
-    // 4. compact: previous best first, then this chunk's candidates
-    if (tid < nprev) { cv[tid] = sh.best_v[tid]; cg[tid] = sh.best_g[tid]; }
-    {
-      int off = sh.woff[warp];
-      for (int base = warp * 32; base < mc; base += kThreads) {
-        const int jj = base + lane;
-        const bool c = jj < mc && vals[jj] >= T;
-        const unsigned bal = __ballot_sync(0xffffffffu, c);
-        const int slot = off + __popc(bal & ((1u << lane) - 1u));
-        if (c) { cv[slot] = vals[jj]; cg[slot] = gids[jj]; }
-        off += __popc(bal);
-      }
-    }
-    __syncthreads();
-    if (tid == 0 && c0 == 0) trace_mark(p.trace, 11);  // compacted
-    // 5. rank by counting; the k winners land in best[rank]
     for (int e = tid; e < tot; e += kThreads) {
       const float ve = cv[e];
       const int32_t ge = cg[e];
@@ -359,7 +364,7 @@ __device__ void topk_node(const TcArgs& a, int seq, int node, int tile_base, int
     }
     __syncthreads();
     if (tid == 0) sh.nbest = min(k, tot);
-    if (tid == 0 && c0 == 0) trace_mark(p.trace, 12);  // ranked
+    if (tid == 0 && c0 == 0) trace_mark(p.trace, 11);  // ranked
     __syncthreads();
   }
   if (tid < k) {
@@ -369,6 +374,7 @@ __device__ void topk_node(const TcArgs& a, int seq, int node, int tile_base, int
   }
   if (a.lse && tid == 0)
     a.lse[(long long)seq * p.n + node] = run_max == -INFINITY ? -INFINITY : run_max + logf(run_sum);
+  __syncthreads();
 }
 
 template <int NT>
@@ -407,6 +413,9 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
   // Everything above overlaps the previous kernel (programmatic dependent
   // launch); the state it produced (n_active, ids) is read only after this.
   pdl_wait();
+  // the next kernel on the stream (typically the next state update) may be
+  // launched now; it waits for this grid's completion before touching state
+  asm volatile("griddepcontrol.launch_dependents;");
   if (tid == 0) trace_mark(p.trace, 1);  // dependency resolved
 
   // Loader pattern: thread t moves 16-B chunk (t & 7) of tile rows lr and
@@ -556,10 +565,54 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
       }
     }
     it += nk;
+
+    // ---------------- split-K reduction, distributed over the tile's S CTAs:
+    // once all S partials of the tile are written (per-tile arrival counter;
+    // the launch is cooperative so the spin is safe), split s sums, in split
+    // order, quads [32 s / S, 32 (s+1) / S) of the tile's rows for every node
+    // and writes the final logits.
+    __threadfence();
+    __syncthreads();
+    if (S > 1) {
+      if (tid == 0) {
+        atomicAdd(&a.counters[2 + tile], 1u);
+        while (ld_acquire(&a.counters[2 + tile]) < (unsigned)S) __nanosleep(20);
+      }
+      __syncthreads();
+    }
+    if (tid == 0 && local == 0) trace_mark(p.trace, 5);  // tile's partials complete
+    {
+      const int q0 = split * (kBM / 4) / S, q1 = (split + 1) * (kBM / 4) / S;
+      const int nq = q1 - q0;
+      for (int item = tid; item < p.n * nq; item += kThreads) {
+        const int c = item / nq, r = 4 * (q0 + item - (item / nq) * nq);
+        if (r >= rows) continue;
+        const float* src = a.part + ((long long)tile * S * NT + c) * kBM + r;
+        float4 x[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < S) x[q] = __ldcg(reinterpret_cast<const float4*>(src + (long long)q * NT * kBM));
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < S) { acc.x += x[q].x; acc.y += x[q].y; acc.z += x[q].z; acc.w += x[q].w; }
+        for (int q = 8; q < S; ++q) {
+          const float4 y = __ldcg(reinterpret_cast<const float4*>(src + (long long)q * NT * kBM));
+          acc.x += y.x; acc.y += y.y; acc.z += y.z; acc.w += y.w;
+        }
+        float* dst = a.zl + ((long long)seq * p.n + c) * p.max_ids + row0 + r;
+        if (((uintptr_t)dst & 15) == 0 && r + 4 <= rows) {
+          __stcg(reinterpret_cast<float4*>(dst), acc);
+        } else {
+          const float vv[4] = {acc.x, acc.y, acc.z, acc.w};
+          for (int i = 0; i < 4 && r + i < rows; ++i) __stcg(dst + i, vv[i]);
+        }
+      }
+    }
   }
 
-  // ---------------- grid barrier: every partial tile written
-  if (tid == 0) trace_mark(p.trace, 5);  // epilogue done
+  // ---------------- grid barrier: every logit reduced
+  if (tid == 0) trace_mark(p.trace, 6);  // reduction done
   __threadfence();
   tc_fence_before();
   __syncthreads();
@@ -568,21 +621,20 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
     atomicAdd(&a.counters[0], 1u);
     if ((int)blockIdx.x < tasks)  // CTAs with top-k work wait for everyone
       while (ld_acquire(&a.counters[0]) < (unsigned)G) __nanosleep(32);
-    trace_mark(p.trace, 6);  // grid barrier passed
+    trace_mark(p.trace, 12);  // grid barrier passed
   }
   __syncthreads();
 
   // ---------------- top-k: (sequence, node) tasks over the CTAs
   {
-    int tseq = 0, ttile0 = 0, tm = sh_m0;
+    int tseq = 0, tm = sh_m0;
     for (int t = blockIdx.x; t < tasks; t += G) {
       const int sq = t / p.n, node = t - (t / p.n) * p.n;
       while (tseq < sq) {
-        ttile0 += (tm + kBM - 1) / kBM;
         ++tseq;
         tm = clamp_nact(p, tseq);
       }
-      topk_node<NT>(a, sq, node, ttile0, S, smem, tsh);
+      topk_node<NT>(a, sq, node, tm, smem, tsh);
     }
   }
 
@@ -594,9 +646,9 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
     sh_tiles = (old == (unsigned)G - 1) ? 1 : 0;
   }
   __syncthreads();
-  if (sh_tiles && tid == 0) {  // the last CTA: every other CTA has passed all its waits
-    a.counters[0] = 0u;
-    a.counters[1] = 0u;
+  if (sh_tiles) {  // the last CTA: every other CTA has passed all its waits
+    for (int t = tid; t < tiles; t += kThreads) a.counters[2 + t] = 0u;
+    if (tid == 0) { a.counters[0] = 0u; a.counters[1] = 0u; }
     __threadfence();
   }
   tc_fence_before();
@@ -608,7 +660,7 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
 }
 
 struct ScratchLayout {
-  size_t counters, part, total;
+  size_t counters, part, zl, total;
 };
 
 inline ScratchLayout scratch_layout(int batch, int max_ids, int n, int nt) {
@@ -619,6 +671,7 @@ inline ScratchLayout scratch_layout(int batch, int max_ids, int n, int nt) {
   size_t off = 0;
   L.counters = off; off += al(sizeof(unsigned) * (2 + max_tiles));
   L.part = off;     off += al(units_cap * nt * kBM * sizeof(float));
+  L.zl = off;       off += al((size_t)batch * n * max_ids * sizeof(float));
   L.total = off;
   return L;
 }
@@ -644,6 +697,7 @@ cudaError_t launch_nt(const HeadProblem& p, int k, float* topk_logit, int32_t* t
   a.p = p;
   a.counters = (unsigned*)(sc + L.counters);
   a.part = (float*)(sc + L.part);
+  a.zl = p.logits ? p.logits : (float*)(sc + L.zl);
   a.topk_logit = topk_logit;
   a.topk_id = topk_id;
   a.lse = lse;

@@ -5,8 +5,8 @@
 // One CTA per (sequence, node).  Exact radix select on an order-preserving
 // 32-bit key (12 + 12 + 8 bits, early exit as soon as the threshold bin is
 // taken whole), then the <= 32 winners are ordered by (value desc, id asc) with
-// a warp bitonic sort.  Exact value ties at the threshold are broken by
-// ascending position in I == ascending global id (I is sorted, Q4/Q10).
+// a warp bitonic sort.  Exact value ties at the threshold are resolved by a
+// second radix select over the global ids (smallest ids first, Q10).
 #include <math.h>
 
 #include "common.cuh"
@@ -151,24 +151,53 @@ __global__ void __launch_bounds__(kSelThreads) select_topk_kernel(HeadProblem p,
   }
   __syncthreads();
   if (!all_in) {
-    // exact ties at the threshold: take the first krem in index (= id) order
-    const int n_gt = sh_n;
-    int taken = 0;
-    for (int base = 0; base < m && taken < krem; base += bs) {
-      const int j = base + tid;
-      bool tie = false;
-      uint32_t key = 0u;
-      if (j < m) {
-        key = float_key(vals[j]);
-        tie = (key & pmask) == prefix;
+    // Exact value ties at the threshold: take the krem smallest global ids
+    // among them (Q10; ids[] is a slot table, not sorted) -- a second radix
+    // select, over the ids, restricted to the tied elements.
+    const uint32_t tie_key = prefix;  // all 32 bits resolved
+    uint32_t gpre = 0u, gmask = 0u;
+    int need = krem;
+    bool gall = false;
+    for (int ps = 0; ps < 3 && !gall; ++ps) {
+      const int nb = 1 << nbits[ps];
+      const uint32_t mask = (uint32_t)nb - 1u;
+      const int shift = shifts[ps];
+      for (int b = tid; b < nb; b += bs) hist[b] = 0;
+      __syncthreads();
+      for (int j = tid; j < m; j += bs) {
+        const uint32_t g = (uint32_t)ids[j];
+        if (float_key(vals[j]) == tie_key && (g & gmask) == gpre) atomicAdd(&hist[(g >> shift) & mask], 1);
       }
-      int tot;
-      int r = taken + block_exclusive_scan(tie ? 1 : 0, sh_scan, &tot);
-      if (tie && r < krem) {
-        cand_key[n_gt + r] = key;
-        cand_idx[n_gt + r] = j;
+      __syncthreads();
+      const int per = nb / bs;
+      const int lo = tid * per;
+      int sv = 0;
+      for (int b = lo; b < lo + per; ++b) sv += hist[b];
+      int T;
+      const int below = block_exclusive_scan(sv, sh_scan, &T);
+      if (below < need && below + sv >= need) {
+        int acc = below;
+        for (int b = lo; b < lo + per; ++b) {
+          if (acc + hist[b] >= need) { sh_bin = b; sh_above = acc; break; }
+          acc += hist[b];
+        }
       }
-      taken += tot;
+      __syncthreads();
+      const int b = sh_bin;
+      need -= sh_above;
+      gpre |= (uint32_t)b << shift;
+      gmask |= mask << shift;
+      gall = hist[b] == need;
+      __syncthreads();
+    }
+    for (int j = tid; j < m; j += bs) {
+      const uint32_t key = float_key(vals[j]);
+      const uint32_t g = (uint32_t)ids[j] & gmask;
+      if (key == tie_key && (g < gpre || g == gpre)) {
+        const int slot = atomicAdd(&sh_n, 1);
+        cand_key[slot] = key;
+        cand_idx[slot] = j;
+      }
     }
     __syncthreads();
   }

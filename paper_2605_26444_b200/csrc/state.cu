@@ -6,8 +6,11 @@
 //   ring[W]  the last W stream slots (slot = position % W),
 //   cnt[V]   how often each id occurs in the window,
 //   bitmap   bit g set  <=>  cnt[g] > 0        (I = Unique(Suffix(S, W)), Eq. 5)
-// and finally recompacts I into ids[] in ascending id by a block prefix sum
-// over the bitmap.  Everything stays on the device; no host sync.
+// and keeps I in ids[0, n_active) as a stable slot table (pos[g] = slot of g):
+// the general path (init, long lists, rule R2) recompacts ascending by a block
+// prefix sum over the bitmap; the per-step fast path changes only the slots of
+// the ids that leave / enter the window (O(changes), not O(V)).  Everything
+// stays on the device; no host sync.
 //
 // tuple(.) deduplication (first occurrence within one list) uses first[V]:
 // atomicMin of the list position per id, then "keep iff first[e] == i".
@@ -171,7 +174,10 @@ __device__ void compact(const StateView& sv, int seq, int* sh_scan) {
       int bit = __ffs(b) - 1;
       b &= b - 1;
       int32_t l = (w << 5) + bit;
-      if (off < sv.w_max) ids[off] = sv.n_shards <= 1 ? l : l * sv.n_shards + sv.rank;
+      if (off < sv.w_max) {
+        ids[off] = sv.n_shards <= 1 ? l : l * sv.n_shards + sv.rank;
+        if (sv.pos) sv.pos[(long long)seq * sv.v_local + l] = off;
+      }
       ++off;
     }
   }
@@ -214,25 +220,51 @@ __global__ void __launch_bounds__(512) state_append_kernel(AppendArgs args) {
   }
 }
 
-// Per-step fast path of a2 (rule R1, no reset, both lists together <= 512
-// ids and <= W_max, W_max <= 8192): one CTA per sequence.  The sequence's
-// bitmap and the new ids are staged in shared memory; tuple(.) dedup is a
-// shared-memory hash (min position per (list, id)); window counts are updated
-// with returning atomics (all decrements, then all increments), so the bit
-// flips are known without re-reading cnt; I is recompacted into shared memory
-// and written back with coalesced stores.  Global round trips: {meta, bitmap,
-// lists} -> ring slots -> decrements -> increments.
+// Per-step fast path of a2 (rule R1, no reset, both lists together <= 512 ids
+// and <= W_max): one CTA per sequence, O(changes) work.
+//  * tuple(.) dedup: shared-memory hash of (list, id) -> first position;
+//  * the evicted ring slots are read, and the net window-count change of every
+//    touched id (appends - evictions) is formed in a shared-memory hash, so one
+//    returning atomicAdd per distinct id tells which ids leave I (count -> 0)
+//    and which enter it (0 -> count);
+//  * slot table (pos[g] = slot of g): entering ids take the slots of leaving
+//    ids, extra entries are appended, surplus holes are refilled from the tail,
+//    so ids[0, n_active) stays dense and every other id keeps its slot.
+// Global round trips: {meta, lists} -> ring slots -> count atomics -> slots of
+// the leaving ids (-> ids of the tail movers when I shrinks).
 constexpr int kFastThreads = 512;
-constexpr int kFastMaxW = 8192;
 constexpr int kHashSlots = 2048;
 
+__device__ __forceinline__ int hash_slot(int32_t key) {
+  return (int)(((uint32_t)key * 2654435761u) >> 21) & (kHashSlots - 1);
+}
+
+// Insert `key` (>= 0) into an open-addressing table; returns its slot.
+__device__ __forceinline__ int hash_insert(int32_t* keys, int32_t key) {
+  int h = hash_slot(key);
+  while (true) {
+    const int32_t old = atomicCAS(&keys[h], -1, key);
+    if (old == -1 || old == key) return h;
+    h = (h + 1) & (kHashSlots - 1);
+  }
+}
+
 __global__ void __launch_bounds__(kFastThreads) state_update_fast_kernel(AppendArgs args, unsigned long long* trace) {
-  extern __shared__ uint32_t dyn[];
-  __shared__ int32_t hkey[kHashSlots];
-  __shared__ int32_t hpos[kHashSlots];
+  __shared__ int32_t hkey[kHashSlots];   // dedup table, then net-delta table
+  __shared__ int32_t hval[kHashSlots];
+  __shared__ int32_t leave[kFastThreads];  // local ids leaving I
+  __shared__ int32_t enter[kFastThreads];  // local ids entering I
+  __shared__ int32_t hole[kFastThreads];   // their former slots
+  __shared__ int32_t mover_slot[kFastThreads];
+  __shared__ int32_t low_hole[kFastThreads];
+  __shared__ unsigned char tail_hole[kFastThreads];
   __shared__ int sh_scan[40];
   __shared__ long long sh_total;
-  __shared__ int sh_err;
+  __shared__ int sh_nact, sh_err, sh_nl, sh_ne, sh_nm, sh_nh;
+  // Programmatic dependent launch: this kernel may start while the previous
+  // kernel on the stream (e.g. the last head call) is still running; it must
+  // not touch the state before that kernel has completed.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (threadIdx.x == 0) trace_mark(trace, 9);  // state: start
   // let the dependent head kernel get resident and run its prologue meanwhile
   asm volatile("griddepcontrol.launch_dependents;");
@@ -240,101 +272,98 @@ __global__ void __launch_bounds__(kFastThreads) state_update_fast_kernel(AppendA
   const int seq = args.seq0 + blockIdx.x;
   const int tid = threadIdx.x;
   const int W = sv.w_max;
-  uint32_t* bm_s = dyn;                                  // [words]
-  int32_t* ids_s = reinterpret_cast<int32_t*>(dyn + sv.words);  // [W]
   const int la = (int)args.a.len, lb = (int)args.b.len;
   const int L = la + lb;
   uint32_t* bm = sv.bitmap + (long long)seq * sv.words;
   int32_t* ring = sv.ring + (long long)seq * W;
   int32_t* cnt = sv.cnt + (long long)seq * sv.v_local;
-  if (tid == 0) { sh_total = sv.meta[seq].total; sh_err = 0; }
+  int32_t* pos = sv.pos + (long long)seq * sv.v_local;
+  int32_t* ids = sv.ids + (long long)seq * W;
+  if (tid == 0) {
+    sh_total = sv.meta[seq].total;
+    sh_nact = sv.meta[seq].n_active;
+    sh_err = 0; sh_nl = 0; sh_ne = 0; sh_nm = 0; sh_nh = 0;
+  }
   int32_t e = -1;
   if (tid < la) e = args.a.ptr[(long long)(seq - args.seq0) * args.a.seq_stride + tid];
   else if (tid < L) e = args.b.ptr[(long long)(seq - args.seq0) * args.b.seq_stride + (tid - la)];
-  {
-    uint32_t tmp[32];  // all bitmap loads of this thread in flight at once (<= 16384 words)
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const int w = tid + i * kFastThreads;
-      if (w < sv.words) tmp[i] = bm[w];
-    }
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const int w = tid + i * kFastThreads;
-      if (w < sv.words) bm_s[w] = tmp[i];
-    }
-  }
-  for (int h = tid; h < kHashSlots; h += kFastThreads) { hkey[h] = -1; hpos[h] = 0x7fffffff; }
+  for (int h = tid; h < kHashSlots; h += kFastThreads) { hkey[h] = -1; hval[h] = 0x7fffffff; }
   __syncthreads();
-  if (tid == 0) trace_mark(trace, 10);  // state: bitmap + lists staged
-  // tuple(.): keep the first occurrence of every id within its own list
+  if (tid == 0) trace_mark(trace, 10);  // state: lists staged
+  // ---- tuple(.): keep the first occurrence of every id within its own list
   const bool valid = tid < L && e >= 0 && e < sv.vocab;
   if (tid < L && !valid) sh_err = 1;
-  int slot_h = -1;
+  int hs = -1;
   if (valid) {
-    const int32_t key = e * 2 + (tid < la ? 0 : 1);
-    int h = (int)(((uint32_t)key * 2654435761u) >> 21) & (kHashSlots - 1);
-    while (true) {
-      const int32_t old = atomicCAS(&hkey[h], -1, key);
-      if (old == -1 || old == key) break;
-      h = (h + 1) & (kHashSlots - 1);
-    }
-    atomicMin(&hpos[h], tid);
-    slot_h = h;
+    hs = hash_insert(hkey, e * 2 + (tid < la ? 0 : 1));
+    atomicMin(&hval[hs], tid);
   }
   __syncthreads();
-  const bool keep = valid && hpos[slot_h] == tid;
+  const bool keep = valid && hval[hs] == tid;
   int nk;
-  const int pos = block_exclusive_scan(keep ? 1 : 0, sh_scan, &nk);
+  const int sp = block_exclusive_scan(keep ? 1 : 0, sh_scan, &nk);
   const long long total = sh_total;
-  int slot = (int)(total % W) + pos;  // pos < W: one wrap at most
+  int slot = (int)(total % W) + sp;  // sp < W: one wrap at most
   if (slot >= W) slot -= W;
   int32_t old = -1;
-  if (keep && total + pos >= W) old = ring[slot];
-  // decrements for the evicted slots
+  if (keep && total + sp >= W) old = ring[slot];
+  if (keep) ring[slot] = e;
+  for (int h = tid; h < kHashSlots; h += kFastThreads) { hkey[h] = -1; hval[h] = 0; }
+  __syncthreads();
   if (tid == 0) trace_mark(trace, 11);  // state: ring slots read
-  if (old >= 0 && is_local(sv, old)) {
-    const int32_t l = local_of(sv, old);
-    if (atomicSub(&cnt[l], 1) == 1) atomicAnd(&bm_s[l >> 5], ~(1u << (l & 31)));
-  }
+  // ---- net window-count change per touched local id
+  if (old >= 0 && is_local(sv, old)) atomicSub(&hval[hash_insert(hkey, local_of(sv, old))], 1);
+  if (keep && is_local(sv, e)) atomicAdd(&hval[hash_insert(hkey, local_of(sv, e))], 1);
   __syncthreads();
-  // increments for the appended ids
-  if (tid == 0) trace_mark(trace, 12);  // state: decrements done
-  if (keep) {
-    ring[slot] = e;
-    if (is_local(sv, e)) {
-      const int32_t l = local_of(sv, e);
-      if (atomicAdd(&cnt[l], 1) == 0) atomicOr(&bm_s[l >> 5], 1u << (l & 31));
+  for (int h = tid; h < kHashSlots; h += kFastThreads) {
+    const int32_t l = hkey[h], dlt = hval[h];
+    if (l < 0 || dlt == 0) continue;
+    const int32_t before = atomicAdd(&cnt[l], dlt);
+    const int32_t after = before + dlt;
+    if (before > 0 && after == 0) {
+      atomicAnd(&bm[l >> 5], ~(1u << (l & 31)));
+      leave[atomicAdd(&sh_nl, 1)] = l;
+    } else if (before == 0 && after > 0) {
+      atomicOr(&bm[l >> 5], 1u << (l & 31));
+      enter[atomicAdd(&sh_ne, 1)] = l;
     }
   }
   __syncthreads();
-  if (tid == 0) trace_mark(trace, 13);  // state: increments done
-  // write the bitmap back; recompact I (ascending) into shared memory
-  for (int w = tid; w < sv.words; w += kFastThreads) bm[w] = bm_s[w];
-  const int per = (sv.words + kFastThreads - 1) / kFastThreads;
-  const int w0 = tid * per, w1 = min(sv.words, w0 + per);
-  int c = 0;
-  for (int w = w0; w < w1; ++w) c += __popc(bm_s[w]);
-  int n;
-  int off = block_exclusive_scan(c, sh_scan, &n);
-  if (tid == 0) trace_mark(trace, 15);  // state: bitmap written back, counts scanned
-  for (int w = w0; w < w1; ++w) {
-    uint32_t b = bm_s[w];
-    while (b) {
-      const int bit = __ffs(b) - 1;
-      b &= b - 1;
-      const int32_t l = (w << 5) + bit;
-      if (off < W) ids_s[off] = sv.n_shards <= 1 ? l : l * sv.n_shards + sv.rank;
-      ++off;
+  if (tid == 0) trace_mark(trace, 12);  // state: counts updated
+  // ---- slot table
+  const int nl = sh_nl, ne = sh_ne;
+  const int n_old = sh_nact, n_new = n_old - nl + ne;
+  if (tid < nl) hole[tid] = pos[leave[tid]];
+  if (tid < n_old - n_new) tail_hole[tid] = 0;
+  __syncthreads();
+  const int32_t gmul = sv.n_shards <= 1 ? 1 : sv.n_shards, gadd = sv.n_shards <= 1 ? 0 : sv.rank;
+  if (tid < ne) {  // entering ids: a freed slot, or a new slot at the end
+    const int s2 = tid < nl ? hole[tid] : n_old + (tid - nl);
+    ids[s2] = enter[tid] * gmul + gadd;
+    pos[enter[tid]] = s2;
+  }
+  if (nl > ne) {
+    // I shrinks by d = nl - ne: holes hole[ne..nl) below n_new are refilled
+    // with the live entries of the tail [n_new, n_old)
+    const int d = nl - ne;
+    if (tid >= ne && tid < nl) {
+      const int h = hole[tid];
+      if (h >= n_new) tail_hole[h - n_new] = 1;
+      else low_hole[atomicAdd(&sh_nh, 1)] = h;
+    }
+    __syncthreads();
+    if (tid < d && !tail_hole[tid]) mover_slot[atomicAdd(&sh_nm, 1)] = n_new + tid;
+    __syncthreads();
+    if (tid < sh_nm) {  // sh_nm == sh_nh; any pairing works
+      const int32_t g = ids[mover_slot[tid]];
+      const int dst = low_hole[tid];
+      ids[dst] = g;
+      pos[local_of(sv, g)] = dst;
     }
   }
-  __syncthreads();
-  int32_t* ids = sv.ids + (long long)seq * W;
-  const int nn = min(n, W);
-  for (int j = tid; j < nn; j += kFastThreads) ids[j] = ids_s[j];  // coalesced
   if (tid == 0) {
     sv.meta[seq].total = total + nk;
-    sv.meta[seq].n_active = n;
+    sv.meta[seq].n_active = n_new;
     if (sh_err) sv.meta[seq].err |= 1;
     trace_mark(trace, 14);  // state: done
   }
@@ -353,20 +382,28 @@ cudaError_t launch_state_append(const StateView& sv, int seq0, int nseq, int res
   args.a = ListArg{a, a_len, a_stride, a_dedup};
   args.b = ListArg{b, b_len, b_stride, b_dedup};
   const long long L = (a ? a_len : 0) + (b ? b_len : 0);
-  if (!reset && sv.rule == 0 && a_dedup && b_dedup && L <= kFastThreads && L <= sv.w_max &&
-      sv.words <= 16384 && sv.w_max <= kFastMaxW) {
+  if (!reset && sv.rule == 0 && sv.pos && a_dedup && b_dedup && L <= kFastThreads && L <= sv.w_max) {
     if (!a) args.a.len = 0;
     if (!b) args.b.len = 0;
-    const size_t smem = sizeof(uint32_t) * ((size_t)sv.words + (size_t)sv.w_max);
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(state_update_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (16384 + kFastMaxW) * (int)sizeof(uint32_t));
-      if (e != cudaSuccess) return e;
-      attr = true;
+    const size_t smem = 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nseq);
+    cfg.blockDim = dim3(kFastThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    unsigned long long* tr = trace_buffer();
+    cudaError_t e = cudaLaunchKernelEx(&cfg, state_update_fast_kernel, args, tr);
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      state_update_fast_kernel<<<nseq, kFastThreads, smem, stream>>>(args, tr);
+      e = cudaGetLastError();
     }
-    state_update_fast_kernel<<<nseq, kFastThreads, smem, stream>>>(args, trace_buffer());
-    return cudaGetLastError();
+    return e;
   }
   state_append_kernel<<<nseq, 512, 0, stream>>>(args);
   return cudaGetLastError();

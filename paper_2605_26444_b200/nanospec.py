@@ -49,8 +49,8 @@ def head_scratch_bytes(batch, max_ids, n_nodes) -> int:
 class ActiveVocab:
     """GPU-resident candidate-stream state for `batch` sequences (a1/a2).
 
-    I = Unique(Suffix(S, W_max)) (Eq. 5) kept as a bitmap + ascending id
-    list entirely in device memory."""
+    I = Unique(Suffix(S, W_max)) (Eq. 5) kept as a bitmap + a stable
+    slot table of ids entirely in device memory."""
 
     def __init__(self, vocab: int, w_max: int, batch: int = 1, rule: str = "window", shard_rank: int = 0,
                  n_shards: int = 1, device=None):
@@ -112,7 +112,9 @@ class ActiveVocab:
                 "nanospec_state_update_batch")
 
     def read(self, seq: int) -> dict:
-        """Synchronises the current stream; host copies of sequence `seq`'s state."""
+        """Synchronises the current stream; host copies of sequence `seq`'s state.
+        `ids` is I in canonical ascending order, `slots` the device slot table
+        (the row order of the head's debug logits)."""
         import numpy as np
         ids = np.empty(self.w_max, np.int32)
         bm = np.empty(self.words, np.uint32)
@@ -123,7 +125,8 @@ class ActiveVocab:
         N.check(N.lib().nanospec_state_read(self.handle, seq, ids.ctypes.data, ctypes.byref(n), bm.ctypes.data,
                                             ring.ctypes.data, ctypes.byref(total), ctypes.byref(err),
                                             _stream(self.device)), "nanospec_state_read")
-        return dict(ids=ids[: n.value].copy(), n_active=n.value, bitmap=bm, ring=ring, total=total.value,
+        slots = ids[: n.value].copy()
+        return dict(ids=np.sort(slots), slots=slots, n_active=n.value, bitmap=bm, ring=ring, total=total.value,
                     err=err.value)
 
     def check(self) -> int:

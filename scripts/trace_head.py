@@ -15,8 +15,8 @@ import paper_2605_26444_b200 as P  # noqa: E402
 from paper_2605_26444_b200 import _native as N  # noqa: E402
 from synthetic import inputs as SI  # noqa: E402
 
-EVENTS = ["start", "dep_ok", "rowptr", "loads_landed", "mma_done", "epilogue", "grid_bar", "tk_loaded",
-          "topk_done", "tk_thresh", "tk_counted", "tk_compacted", "tk_ranked"]
+EVENTS = ["start", "dep_ok", "rowptr", "loads_landed", "mma_done", "tile_ready", "reduced", "tk_gathered",
+          "topk_done", "tk_thresh", "tk_compacted", "tk_ranked", "grid_bar"]
 
 
 def main():
@@ -63,6 +63,9 @@ def main():
         print(f"=== {mode} (m={args.m}, n={args.n}); event-timed call: "
               f"{np.median([r[0] for r in rows]):.2f} us median of {args.reps}")
         ev_us, t, t0 = rows[-1]
+        print("  candidates per task:", sorted(int(x) for x in t[:, 15] if x > 0)[:12], "...")
+        t[:, 13:16] = 0
+        t[:, 13] = 0
 
         for e, name in enumerate(EVENTS):
             col = t[:, e]
@@ -81,7 +84,7 @@ def trace_state():
     st = P.ActiveVocab(V, 3072, device=dev)
     st.init(0, torch.as_tensor(prompt, device=dev))
     trace = torch.zeros(256 * 16, dtype=torch.int64, device=dev)
-    names = ["start", "staged", "ring_read", "decrements", "increments", "done", "scanned"]
+    names = ["start", "staged", "ring_read", "counts", "-", "done"]
     for i, (d, v) in enumerate(ups):
         dd, vv = torch.as_tensor(d, device=dev), torch.as_tensor(v, device=dev)
         torch.cuda.synchronize()
@@ -93,7 +96,7 @@ def trace_state():
         torch.cuda.synchronize()
         N.check(N.lib().nanospec_debug_set_trace(None, 0), "set_trace")
         t = trace.view(256, 16)[0].cpu().numpy().astype(np.int64)
-        rel = [(t[9 + j] - t[9]) / 1e3 for j in range(7)]
+        rel = [(t[9 + j] - t[9]) / 1e3 for j in range(6)]
         print(f"state update {i}: event {e0.elapsed_time(e1) * 1e3:.2f} us; " +
               " ".join(f"{n}={r:.2f}" for n, r in zip(names, rel)))
 

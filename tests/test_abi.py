@@ -43,8 +43,8 @@ def _a(x):
 
 def test_workspace_layout_and_table6_sizes():
     """Per-sequence state = bitmap ceil(V/32)*4 (the paper's 16 KB `token_ids`,
-    T6 P:449) + ids W*4 (12 KB at W=3072) + ring W*4 + cnt V*4 + first V*4 +
-    16-byte meta; independent of context length."""
+    T6 P:449) + ids W*4 (12 KB at W=3072) + ring W*4 + cnt V*4 + pos V*4 +
+    first V*4 + 16-byte meta; independent of context length."""
     gold = json.load(open(os.path.join(ROOT, "tests", "golden", "paper_table6.json")))
     V, W = gold["vocab"], gold["w_max"]
     L = N.lib()
@@ -53,15 +53,15 @@ def test_workspace_layout_and_table6_sizes():
     assert W * 4 == gold["exact_bytes"]["tokens_tensor"]
     assert W * gold["d_model"] * 2 == gold["exact_bytes"]["repack_buf"]  # what one head call reads at |I| = W
     got = L.nanospec_state_workspace_bytes(V, W, 1, 0, 0, 1)
-    assert got == _a(16) + _a(words * 4) + _a(W * 4) * 2 + _a(V * 4) * 2
-    # R2 keeps no cnt array
-    assert L.nanospec_state_workspace_bytes(V, W, 1, 1, 0, 1) == got - _a(V * 4)
+    assert got == _a(16) + _a(words * 4) + _a(W * 4) * 2 + _a(V * 4) * 3
+    # R2 keeps no cnt / pos arrays
+    assert L.nanospec_state_workspace_bytes(V, W, 1, 1, 0, 1) == got - 2 * _a(V * 4)
     # batch scales linearly (one state per sequence)
-    assert L.nanospec_state_workspace_bytes(V, W, 64, 0, 0, 1) >= 64 * (words * 4 + W * 8 + V * 8)
-    # vocab-parallel shard: bitmap/cnt over V_local, first over V
+    assert L.nanospec_state_workspace_bytes(V, W, 64, 0, 0, 1) >= 64 * (words * 4 + W * 8 + V * 12)
+    # vocab-parallel shard: bitmap/cnt/pos over V_local, first over V
     vl = (V - 3 + 7) // 8
     assert L.nanospec_state_workspace_bytes(V, W, 1, 0, 3, 8) == \
-        _a(16) + _a(((vl + 31) // 32) * 4) + _a(W * 4) * 2 + _a(vl * 4) + _a(V * 4)
+        _a(16) + _a(((vl + 31) // 32) * 4) + _a(W * 4) * 2 + _a(vl * 4) * 2 + _a(V * 4)
 
 
 @pytest.mark.parametrize("args", [(0, 10, 1, 0, 0, 1), (10, 0, 1, 0, 0, 1), (10, 10, 0, 0, 0, 1),

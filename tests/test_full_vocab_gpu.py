@@ -81,7 +81,7 @@ def test_vocab_parallel_merge(cuda_ok, impl, G):
         st.init(0, pt, prt)
         Wr = W[r::G].contiguous()
         v, i, l, zz = draft_logits_topk(st, Wr, H.reshape(1, n, d), k, impl=impl, debug_logits=True)
-        ids_r = st.read(0)["ids"]
+        ids_r = st.read(0)["slots"]
         cl.append(v[0].clone())
         ci.append(i[0].clone())
         cls.append(l[0].clone())

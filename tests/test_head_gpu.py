@@ -44,7 +44,8 @@ def _run(st, W, H, k, impl):
 
 def _full_check(st, W, Wbits, H, k, impl, what, exact=False):
     got = st.read(0)
-    ids = got["ids"]
+    ids = got["slots"]  # device row order of the debug logits
+    assert np.array_equal(np.sort(ids), got["ids"])
     z_ref, A = O.logits(Wbits, SI.bf16_bits(H), ids)
     v, i, l, z = _run(st, W, H, k, impl)
     m = len(ids)
@@ -146,7 +147,7 @@ def test_exact_one_hot_zero_and_duplicates(cuda_ok, impl):
     for i, c in enumerate((0, 5, 300)):
         H[i + 1, c] = 1.0  # one-hot rows: z_j = W[I_j][c] exactly
     z_ref, ids_o, v, i, l = _full_check(st, W, Wb, H, 32, impl, "one-hot/zero", exact=True)
-    assert i[0].tolist() == sorted(ids_o.tolist())[:32]  # h = 0: all tie -> smallest ids
+    assert i[0].tolist() == sorted(ids_o.tolist())[:32]  # h = 0: all tie -> smallest ids (whatever the slot order)
     assert abs(l[0] - np.log(len(ids_o))) < 1e-5
     Hr = SI.bf16_hidden(6, d, seed=9, device="cuda")
     _, _, _, zz = _run(st, W, Hr, 32, impl)
@@ -176,7 +177,7 @@ def test_batch_of_sequences(cuda_ok, llama, impl):
     v, i, l, _ = draft_logits_topk(st, W, H, k, impl=impl)
     torch.cuda.synchronize()
     for b in range(B):
-        ids = st.read(b)["ids"]
+        ids = st.read(b)["slots"]
         z_ref, A = O.logits(Wb, SI.bf16_bits(H[b]), ids)
         v_ref, id_ref = O.topk(z_ref, ids, k)
         check_topk(v[b].cpu().numpy(), i[b].cpu().numpy(), z_ref, A, ids, v_ref, id_ref, f"seq {b}")
