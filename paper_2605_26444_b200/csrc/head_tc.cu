@@ -11,26 +11,28 @@
 // (the UMMA K-major SW128 layout), so weight bytes cross HBM exactly once.
 //
 // Contraction.  UMMA M = 128 active rows (A), N = NT >= n nodes (B, zero
-// padded), K = 64 per pipeline stage; D in TMEM (NT fp32 columns).  T =
-// sum_b ceil(n_active_b / 128) tiles are read from device memory (no host
-// sync); every tile is split along K into S = max(1, floor(#SMs / T)) uniform
-// chunks so that ~all SMs stream.  Each (tile, chunk) unit writes its fp32
-// partial tile to L2-resident scratch.
+// padded), K = 64 per pipeline stage; D in TMEM (NT fp32 columns).  A launch
+// covers tiles_g = batch * ceil(max_ids / 128) row tiles (tiles past a
+// sequence's n_active, read from device memory, exit at once).  With
+// tiles_g < #SMs every tile is split along K into S = min(8, #SMs / tiles_g)
+// chunks handled by the S CTAs of one thread-block cluster, so ~all SMs stream.
 //
-// Top-k, two levels spread over all CTAs.  Level 1: as soon as the S partials
-// of a tile are written (per-tile arrival counter; the launch is cooperative so
-// all CTAs are co-resident and the spin is safe), the tile's S CTAs split its
-// (tile, node) pairs; one warp per pair sums the S partials of the 128 rows in
-// split order (fixed order -> equal rows give bit-equal logits) and keeps the
-// pair's exact top-k (k arg-max rounds over (value desc, id asc) packed into
-// 64-bit keys) plus (max, sum exp) for the lse.  Level 2, after one grid
-// barrier: one CTA per (sequence, node) merges the ceil(|I|/128) * k level-1
-// candidates the same way and combines the lse partials.
+// Reduction + top-k, no grid-wide synchronisation:
+//  1. each CTA drains its partial tile from TMEM into its own shared memory;
+//     after a cluster barrier, CTA s sums -- over distributed shared memory, in
+//     split order (fixed order: equal rows give bit-equal logits) -- the 128
+//     rows of nodes s, s+S, ...;
+//  2. level 1, one warp per (tile, node): exact top-k of the 128 logits
+//     (threshold = k-th largest lane maximum, compaction, rank by counting)
+//     and (max, sum exp) for the lse, written to L2-resident scratch;
+//  3. level 2: a per-(sequence, node) arrival counter; the warp that brings it
+//     to ceil(n_active / 128) merges that node's sorted per-tile lists
+//     (threshold = k-th largest list head, rank by counting) and combines the
+//     lse partials -- the last arriver finishes the node, nobody waits.
 //
 // Warp roles (544 threads): warps 0-15 load (cp.async) and drain TMEM (warp w
 // reads TMEM lanes 32*(w%4).. and a quarter of the columns); warp 16 allocates
-// TMEM and one lane issues the MMAs.  All 17 warps run the top-k phase (enough
-// warps per scheduler to hide shared-memory and shuffle latencies).
+// TMEM and one lane issues the MMAs.  All 17 warps run the reduction / top-k.
 #include <math.h>
 
 #include "common.cuh"
@@ -48,21 +50,24 @@ constexpr int kThreads = kLoaders + 32;   // + one MMA-issue warp
 constexpr int kWarps = kThreads / 32;
 constexpr int kSmemBudget = 192 * 1024;
 constexpr int kMaxSMs = 256;
-constexpr int kCandCap = 1024;    // candidates kept for the exact ranking
 constexpr int kMaxK = 32;
+constexpr int kMaxCluster = 8;    // portable cluster size
+constexpr int kL2Tiles = 64;      // tiles per sequence whose level-2 inputs are fetched in one round trip
 
 struct TcArgs {
   HeadProblem p;
-  float* part;                 // [units][NT][128] fp32 partial tiles (split-K)
-  float* zl;                   // [batch][n][max_ids] reduced logits (the debug output when requested)
-  unsigned* counters;          // [0] grid arrive, [1] grid done, [2 + tile] tile arrivals (zero between launches)
-  float* topk_logit;           // [batch][n][k]
+  uint2* cand;          // [tiles_g][n][k] level-1 lists (float_key, global id), best first
+  float2* tstat;        // [tiles_g][n] (max, sum exp(z - max)) over a tile's rows
+  unsigned* node_ctr;   // [batch * n] level-1 arrivals per (sequence, node); zero between launches
+  float* topk_logit;    // [batch][n][k]
   int32_t* topk_id;
-  float* lse;                  // [batch][n] or null
+  float* lse;           // [batch][n] or null
   int k;
-  int max_tiles;
+  int S;                // K splits per tile == cluster size (1: no cluster, persistent CTAs)
+  int tps;              // tiles per sequence = ceil(max_ids / 128)
 };
 
+// ------------------------------------------------------------------ PTX helpers
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -136,15 +141,38 @@ __device__ __forceinline__ uint32_t ld_acquire(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-// ------------------------------------------------------------------ work split
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Address of the same shared-memory location in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float4 ld_dsmem_v4(uint32_t caddr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(caddr)
+               : "memory");
+  return v;
+}
 __device__ __forceinline__ int clamp_nact(const HeadProblem& p, int b) {
   int m = p.nact_base[(long long)b * p.nact_stride];
   return m < 0 ? 0 : (m > p.max_ids ? p.max_ids : m);
 }
-__device__ __forceinline__ int batch_m0(const HeadProblem& p) { return p.batch > 0 ? clamp_nact(p, 0) : 0; }
-
-
 
 template <int NT>
 struct Cfg {
@@ -153,228 +181,205 @@ struct Cfg {
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStages = (kSmemBudget / kStageBytes) > 8 ? 8 : (kSmemBudget / kStageBytes);
   static constexpr int kTmemCols = NT < 32 ? 32 : NT;
-  static constexpr int kPipeArea = kStages * kStageBytes;
-  static constexpr int kTopkArea = 2 * kCandCap * 4;  // top-k phase staging
-  static constexpr int kStageArea = kPipeArea > kTopkArea ? kPipeArea : kTopkArea;
+  static constexpr int kStageArea = kStages * kStageBytes;
+  // after the MMAs the stage area holds the partial tile P[NT][128] fp32 and a
+  // per-warp scratch for the selections
+  static constexpr int kPBytes = NT * kBM * 4;
+  static constexpr int kWarpScratch = ((kStageArea - kPBytes) / kWarps) / 8 * 8;  // bytes
+  static_assert(kWarpScratch >= kBM * 8, "per-warp scratch");
   static constexpr int kSmemBytes = kStageArea + 1024 /*align*/ + 256 /*barriers*/;
   static_assert(2 * kStages + 3 <= 30, "barrier area");
   static constexpr int kHChunks = NT * 8;                 // 16-B chunks of one H stage
   static constexpr int kColGroups = NT / 16 < 4 ? NT / 16 : 4;  // epilogue column groups
 };
 
-struct TopkSmem {
-  float wmax[kWarps];     // per-warp max, sum exp(v - max), threshold candidate
-  float wsum[kWarps];
-  float wthr[kWarps];
-  float T;                // candidate threshold of the chunk
-  int ncand;
-  int nbest;
-  float best_v[kMaxK];
-  int32_t best_g[kMaxK];
-};
-
-__device__ __forceinline__ bool ranks_before(float va, int32_t ga, float vb, int32_t gb) {
-  const uint32_t ka = float_key(va), kb = float_key(vb);
+__device__ __forceinline__ float key_value(uint32_t kk) {
+  if (kk == 0u) return -INFINITY;  // "none"
+  return __uint_as_float((kk & 0x80000000u) ? (kk & 0x7fffffffu) : ~kk);
+}
+// (value desc, id asc): a before b
+__device__ __forceinline__ bool key_before(uint32_t ka, int32_t ga, uint32_t kb, int32_t gb) {
   return ka > kb || (ka == kb && ga < gb);
 }
-
-// k-th largest (k <= 32) of one float per lane, by counting (ties by lane).
-__device__ __forceinline__ float warp_kth_largest(float x, int k) {
+// k-th largest (1 <= k <= 32) of one key per lane, by counting (ties by lane).
+__device__ __forceinline__ uint32_t warp_kth_key(uint32_t x, int k) {
   const int lane = threadIdx.x & 31;
   int rank = 0;
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
-    const float o = __shfl_sync(0xffffffffu, x, j);
+    const uint32_t o = __shfl_sync(0xffffffffu, x, j);
     rank += (o > x || (o == x && j < lane)) ? 1 : 0;
   }
   const unsigned sel = __ballot_sync(0xffffffffu, rank == k - 1);
   return __shfl_sync(0xffffffffu, x, __ffs(sel) - 1);
 }
 
-// Top-k + lse of one (sequence, node), the whole CTA; every phase runs on all
-// warps in parallel (a single warp executes ~6 cycles per instruction here):
-//  1. each thread cp.async's its rows' S split partials and ids (<= 2 float4
-//     groups per chunk) into its own shared-memory slots -- all in flight at
-//     once, no registers held -- then sums them in split order (fixed order:
-//     equal rows give bit-equal logits) and keeps (max, sum exp) online;
-//  2. per-warp (max, sum exp) and, for k > 16, the k-th largest lane maximum;
-//  3. warp 0 combines the 17 warp summaries: lse partial and a threshold T that
-//     at least k values reach (k <= 16: the k-th largest warp maximum; else the
-//     largest per-warp k-th lane maximum);
-//  4. values >= T (plus the running best) are compacted into shared memory and
-//     ranked by counting (value desc, id asc).
-template <int NT>
-__device__ void topk_node(const TcArgs& a, int seq, int node, int m, uint8_t* smem, TopkSmem& sh) {
+// Rank `cnt` staged (key, gid) candidates by counting and write the k best
+// (best first) to out[0..k); the warp-private scratch holds the candidates.
+__device__ __forceinline__ void warp_rank_write(const uint2* cs, int cnt, int k, uint2* out) {
+  const int lane = threadIdx.x & 31;
+  for (int e = lane; e < cnt; e += 32) {
+    const uint2 me = cs[e];
+    int r = 0;
+    for (int f = 0; f < cnt; ++f) {
+      const uint2 o = cs[f];
+      r += key_before(o.x, (int32_t)o.y, me.x, (int32_t)me.y) ? 1 : 0;
+    }
+    if (r < k) out[r] = me;
+  }
+}
+
+// Level 1 for one (tile, node): the 128 logits of the tile's rows (4 per lane).
+// Writes the tile's sorted top-k (key, gid) -- padded with (0, -1) -- and
+// (max, sum exp) of the valid rows.
+__device__ __forceinline__ void level1(const float (&v)[4], const int32_t (&g)[4], int r0, int rows, int k,
+                                       uint2* scratch, uint2* cand_out, float2* tstat_out) {
+  const int lane = threadIdx.x & 31;
+  uint32_t key[4];
+  uint32_t lmk = 0u;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    key[i] = (r0 + i < rows) ? float_key(v[i]) : 0u;
+    lmk = key[i] > lmk ? key[i] : lmk;
+  }
+  // lse partial
+  const float M = key_value(__reduce_max_sync(0xffffffffu, lmk));
+  float es = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (key[i]) es += __expf(v[i] - M);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
+  // threshold: k-th largest lane maximum (k lanes each own a value >= T)
+  const uint32_t T = warp_kth_key(lmk, k);
+  int cnt = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool c = key[i] != 0u && key[i] >= T;
+    const unsigned bal = __ballot_sync(0xffffffffu, c);
+    if (c) scratch[cnt + __popc(bal & ((1u << lane) - 1u))] = make_uint2(key[i], (uint32_t)g[i]);
+    cnt += __popc(bal);
+  }
+  __syncwarp();
+  if (lane < k) cand_out[lane] = make_uint2(0u, 0xffffffffu);  // padding when rows < k
+  __syncwarp();
+  warp_rank_write(scratch, cnt, k, cand_out);
+  if (lane == 0) *tstat_out = make_float2(M, es);
+}
+
+// Level 2 for one (sequence, node), one warp: merge ntiles sorted lists.
+__device__ void level2(const TcArgs& a, int seq, int node, int tile0, int ntiles, uint2* scratch, int cap) {
   const HeadProblem& p = a.p;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lane = threadIdx.x & 31;
   const int k = a.k;
-  const int32_t* ids = p.ids_base + (long long)seq * p.ids_stride;
   const long long ob = ((long long)seq * p.n + node) * k;
-  float* cv = reinterpret_cast<float*>(smem);
-  int32_t* cg = reinterpret_cast<int32_t*>(cv + kCandCap);
-  constexpr int kChunk = 2 * kThreads * 4;  // rows per chunk
-  if (tid == 0) sh.nbest = 0;
-  float run_max = -INFINITY, run_sum = 0.f;  // online lse over chunks (kept by warp 0 lane 0)
-  for (int c0 = 0; c0 < m; c0 += kChunk) {
-    const int mc = min(kChunk, m - c0);
-    // ---- 1. gather the reduced logits and ids (<= 2 float4 groups per thread, all in flight)
-    float v[8];
-    int32_t g[8];
-    float tm = -INFINITY;
-    {
-      const float* zrow = a.zl + ((long long)seq * p.n + node) * p.max_ids;
-      float4 x[2];
-      int4 gi[2];
+  const uint2* lists = a.cand + ((long long)tile0 * p.n + node) * k;  // list t at lists + t * n * k
+  const long long lstride = (long long)p.n * k;
+  // one round trip: every lane fetches its tiles' (max, sum exp) and list heads
+  float2 st[kL2Tiles / 32];
+  uint32_t head[kL2Tiles / 32];
+  uint32_t mk = 0u;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int jj = 4 * (tid + h * kThreads);
-        const int j = c0 + jj;
-        x[h] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-        gi[h] = make_int4(0, 0, 0, 0);
-        if (jj < mc) {
-          if (((((uintptr_t)(zrow + j)) | ((uintptr_t)(ids + j))) & 15) == 0 && j + 3 < m) {
-            x[h] = __ldcg(reinterpret_cast<const float4*>(zrow + j));
-            gi[h] = __ldcg(reinterpret_cast<const int4*>(ids + j));
-          } else {
-            x[h].x = __ldcg(zrow + j);
-            gi[h].x = __ldg(ids + j);
-            if (j + 1 < m) { x[h].y = __ldcg(zrow + j + 1); gi[h].y = __ldg(ids + j + 1); }
-            if (j + 2 < m) { x[h].z = __ldcg(zrow + j + 2); gi[h].z = __ldg(ids + j + 2); }
-            if (j + 3 < m) { x[h].w = __ldcg(zrow + j + 3); gi[h].w = __ldg(ids + j + 3); }
-          }
-        }
-      }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int jj = 4 * (tid + h * kThreads);
-        const float vv[4] = {x[h].x, x[h].y, x[h].z, x[h].w};
-        const int32_t gg[4] = {gi[h].x, gi[h].y, gi[h].z, gi[h].w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const bool ok = jj + i < mc;
-          v[4 * h + i] = ok ? vv[i] : -INFINITY;
-          g[4 * h + i] = gg[i];
-          if (ok) tm = fmaxf(tm, vv[i]);
-        }
-      }
+  for (int c = 0; c < kL2Tiles / 32; ++c) {
+    const int t = lane + 32 * c;
+    st[c] = make_float2(-INFINITY, 0.f);
+    head[c] = 0u;
+    if (t < ntiles) {
+      st[c] = __ldcg(&a.tstat[(long long)(tile0 + t) * p.n + node]);
+      head[c] = __ldcg(&lists[t * lstride]).x;
     }
-    float ts = 0.f;
-    if (tm != -INFINITY) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) ts += __expf(v[i] - tm);  // exp(-inf) = 0 for padding
-    }
-    if (tid == 0 && c0 == 0) trace_mark(p.trace, 7);  // gathered
-    // ---- 2. per-warp summaries
-    float wm = tm;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
-    float ws = (tm == -INFINITY) ? 0.f : ts * __expf(tm - wm);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ws += __shfl_xor_sync(0xffffffffu, ws, o);
-    const float wt = k > 16 ? warp_kth_largest(tm, k) : -INFINITY;
-    if (lane == 0) { sh.wmax[warp] = wm; sh.wsum[warp] = ws; sh.wthr[warp] = wt; }
-    if (tid == 0) sh.ncand = sh.nbest;  // the running best go first
-    __syncthreads();
-    // ---- 3. every warp combines the 17 warp summaries itself (no extra
-    //         barrier): lse partial (kept by thread 0) and the threshold T
-    float T;
-    {
-      const float x = lane < kWarps ? sh.wmax[lane] : -INFINITY;
-      float M = x;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-      if (warp == 0) {
-        float es = (lane < kWarps && x != -INFINITY) ? sh.wsum[lane] * __expf(x - M) : 0.f;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
-        if (lane == 0 && M != -INFINITY) {
-          const float nm = fmaxf(run_max, M);
-          run_sum = (run_max == -INFINITY ? 0.f : run_sum * __expf(run_max - nm)) + es * __expf(M - nm);
-          run_max = nm;
-        }
-      }
-      if (k <= 16) {
-        // k-th largest warp maximum, by counting over the kWarps lanes
-        int rank = 0;
-#pragma unroll
-        for (int j = 0; j < kWarps; ++j) {
-          const float o = __shfl_sync(0xffffffffu, x, j);
-          rank += (o > x || (o == x && j < lane)) ? 1 : 0;
-        }
-        const unsigned sel = __ballot_sync(0xffffffffu, lane < kWarps && rank == k - 1);
-        T = __shfl_sync(0xffffffffu, x, __ffs(sel) - 1);
-      } else {
-        T = lane < kWarps ? sh.wthr[lane] : -INFINITY;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) T = fmaxf(T, __shfl_xor_sync(0xffffffffu, T, o));
-      }
-      if (sh.nbest == k) T = fmaxf(T, sh.best_v[k - 1]);
-    }
-    if (tid == 0 && c0 == 0) trace_mark(p.trace, 9);  // threshold
-    // ---- 4. compact the values >= T (plus the running best), then rank
-    const int nprev = sh.nbest;
-    if (tid < nprev) { cv[tid] = sh.best_v[tid]; cg[tid] = sh.best_g[tid]; }
-    int cnt = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) cnt += (v[i] != -INFINITY && v[i] >= T) ? 1 : 0;
-    if (cnt) {
-      int slot = atomicAdd(&sh.ncand, cnt);
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-        if (v[i] != -INFINITY && v[i] >= T) {
-          if (slot < kCandCap) { cv[slot] = v[i]; cg[slot] = g[i]; }
-          ++slot;
-        }
-    }
-    __syncthreads();
-    if (tid == 0 && c0 == 0) trace_mark(p.trace, 10);  // compacted
-    const int tot = sh.ncand;
-    if (tid == 0 && c0 == 0 && p.trace) p.trace[(long long)blockIdx.x * kTraceSlots + 15] = tot;
-    if (tot > kCandCap) {
-      // Degenerate ties (e.g. h = 0): exact but slow fallback -- one thread
-      // re-walks the chunk in row order (= ascending id) with a sorted best-k.
-      if (tid == 0) {
-        int nb = sh.nbest;
-        for (int jj = 0; jj < mc; ++jj) {
-          const int j = c0 + jj;
-          const float vv = __ldcg(a.zl + ((long long)seq * p.n + node) * p.max_ids + j);
-          const int32_t gg = __ldg(ids + j);
-          if (nb == k && !ranks_before(vv, gg, sh.best_v[k - 1], sh.best_g[k - 1])) continue;
-          int pos = nb < k ? nb : k - 1;
-          while (pos > 0 && ranks_before(vv, gg, sh.best_v[pos - 1], sh.best_g[pos - 1])) {
-            sh.best_v[pos] = sh.best_v[pos - 1];
-            sh.best_g[pos] = sh.best_g[pos - 1];
-            --pos;
-          }
-          sh.best_v[pos] = vv;
-          sh.best_g[pos] = gg;
-          if (nb < k) ++nb;
-        }
-        sh.nbest = nb;
-      }
-      __syncthreads();
-      continue;
-    }
-    for (int e = tid; e < tot; e += kThreads) {
-      const float ve = cv[e];
-      const int32_t ge = cg[e];
-      int r = 0;
-      for (int f = 0; f < tot; ++f) r += ranks_before(cv[f], cg[f], ve, ge) ? 1 : 0;
-      if (r < k) { sh.best_v[r] = ve; sh.best_g[r] = ge; }
-    }
-    __syncthreads();
-    if (tid == 0) sh.nbest = min(k, tot);
-    if (tid == 0 && c0 == 0) trace_mark(p.trace, 11);  // ranked
-    __syncthreads();
   }
-  if (tid < k) {
-    const bool ok = tid < sh.nbest;
-    a.topk_logit[ob + tid] = ok ? sh.best_v[tid] : -INFINITY;
-    a.topk_id[ob + tid] = ok ? sh.best_g[tid] : -1;
+  for (int t = lane + kL2Tiles; t < ntiles; t += 32) {  // (more than kL2Tiles tiles: rare)
+    const float x = __ldcg(&a.tstat[(long long)(tile0 + t) * p.n + node]).x;
+    const uint32_t kx = x == -INFINITY ? 0u : float_key(x);
+    mk = kx > mk ? kx : mk;
   }
-  if (a.lse && tid == 0)
-    a.lse[(long long)seq * p.n + node] = run_max == -INFINITY ? -INFINITY : run_max + logf(run_sum);
-  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < kL2Tiles / 32; ++c) {
+    const uint32_t kx = st[c].x == -INFINITY ? 0u : float_key(st[c].x);
+    mk = kx > mk ? kx : mk;
+  }
+  const float M = key_value(__reduce_max_sync(0xffffffffu, mk));
+  float es = 0.f;
+#pragma unroll
+  for (int c = 0; c < kL2Tiles / 32; ++c)
+    if (st[c].x != -INFINITY) es += st[c].y * __expf(st[c].x - M);
+  for (int t = lane + kL2Tiles; t < ntiles; t += 32) {
+    const float2 s2 = __ldcg(&a.tstat[(long long)(tile0 + t) * p.n + node]);
+    if (s2.x != -INFINITY) es += s2.y * __expf(s2.x - M);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
+  // threshold: k-th largest list head (k lists each own a value >= T)
+  uint32_t T = 0u;
+  if (ntiles <= 32 && ntiles >= k) T = warp_kth_key(head[0], k);
+  // candidates >= T into the warp scratch; each lane reads its list kChunk
+  // entries at a time (all in flight), stopping once a whole row qualifies nowhere
+  constexpr int kChunk = 8;
+  int cnt = 0;
+  bool overflow = false;
+  for (int t0 = 0; t0 < ntiles; t0 += 32) {
+    const int t = t0 + lane;
+    bool more = true;
+    for (int j0 = 0; j0 < k && more; j0 += kChunk) {
+      uint2 e[kChunk];
+#pragma unroll
+      for (int jj = 0; jj < kChunk; ++jj)
+        e[jj] = (t < ntiles && j0 + jj < k) ? __ldcg(&lists[t * lstride + j0 + jj]) : make_uint2(0u, 0u);
+#pragma unroll
+      for (int jj = 0; jj < kChunk; ++jj) {
+        const bool c = e[jj].x != 0u && e[jj].x >= T;
+        const unsigned bal = __ballot_sync(0xffffffffu, c);
+        if (!bal) { more = false; break; }  // lists are sorted: nothing further qualifies
+        const int slot = cnt + __popc(bal & ((1u << lane) - 1u));
+        if (c && slot < cap) scratch[slot] = e[jj];
+        cnt += __popc(bal);
+      }
+    }
+  }
+  overflow = cnt > cap;
+  __syncwarp();
+  uint2 res = make_uint2(0u, 0xffffffffu);
+  if (!overflow) {
+    uint2* best = scratch + cap - kMaxK;  // (cap > kMaxK + candidates: guarded below)
+    if (cnt + kMaxK <= cap) {
+      if (lane < k) best[lane] = make_uint2(0u, 0xffffffffu);
+      __syncwarp();
+      warp_rank_write(scratch, cnt, k, best);
+      __syncwarp();
+      if (lane < k) res = best[lane];
+    } else {
+      overflow = true;
+    }
+  }
+  if (overflow) {
+    // many candidates (e.g. the dense [0, V) comparator): k rounds of a warp
+    // arg-max over the list heads (heads kept in the scratch as positions)
+    int* hpos = reinterpret_cast<int*>(scratch);
+    for (int t = lane; t < ntiles; t += 32) hpos[t] = 0;
+    __syncwarp();
+    for (int r = 0; r < k; ++r) {
+      uint32_t bk = 0u;
+      int32_t bg = 0x7fffffff;
+      int bt = -1;
+      for (int t = lane; t < ntiles; t += 32) {
+        if (hpos[t] >= k) continue;
+        const uint2 e = __ldcg(&lists[t * lstride + hpos[t]]);
+        if (e.x != 0u && key_before(e.x, (int32_t)e.y, bk, bg)) { bk = e.x; bg = (int32_t)e.y; bt = t; }
+      }
+      const uint32_t wk = __reduce_max_sync(0xffffffffu, bk);
+      if (wk == 0u) break;
+      const int32_t wg = (int32_t)__reduce_min_sync(0xffffffffu, bk == wk ? (uint32_t)bg : 0x7fffffffu);
+      if (bk == wk && bg == wg && bt >= 0) hpos[bt] += 1;
+      __syncwarp();
+      if (lane == r) res = make_uint2(wk, (uint32_t)wg);
+    }
+  }
+  if (lane < k) {
+    a.topk_logit[ob + lane] = res.x ? key_value(res.x) : -INFINITY;
+    a.topk_id[ob + lane] = res.x ? (int32_t)res.y : -1;
+  }
+  if (a.lse && lane == 0) a.lse[(long long)seq * p.n + node] = M == -INFINITY ? -INFINITY : M + logf(es);
 }
 
 template <int NT>
@@ -386,14 +391,14 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStageArea);
   // bars[0..S) full, [S..2S) empty, [2S] tmem_full, [2S+1] tmem_empty
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::kStages + 2);
-  __shared__ int sh_tiles, sh_S, sh_m0;
-  __shared__ TopkSmem tsh;
+  __shared__ int32_t ids_s[kBM];   // the unit's row ids
+  __shared__ int sh_last[kWarps];
 
   const HeadProblem& p = a.p;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int KB = p.d / kBK;
-  const int G = gridDim.x;
+  const int S = a.S;
 
   if (tid == 0) trace_mark(p.trace, 0);  // start
   if (tid == 0) {
@@ -417,78 +422,47 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
   // launched now; it waits for this grid's completion before touching state
   asm volatile("griddepcontrol.launch_dependents;");
   if (tid == 0) trace_mark(p.trace, 1);  // dependency resolved
-
-  // Loader pattern: thread t moves 16-B chunk (t & 7) of tile rows lr and
-  // lr + 64 (lr = t >> 3) of every W stage, and of H rows lr + 64 i < NT.
-  const int lr = tid >> 3;
-  const uint32_t swz = (uint32_t)(((tid & 7) ^ (lr & 7)) << 4);
-  // Speculative first unit, assuming every sequence holds max_ids active rows:
-  // its id loads go out together with the n_active reads (re-issued below if
-  // the guess is wrong).
-  const int tps_g = (p.max_ids + kBM - 1) / kBM;
-  const int tiles_g = p.batch * tps_g;
-  const int S_g = (tiles_g >= G) ? 1 : min(KB, G / tiles_g);
-  int32_t gid_pre[2] = {0, 0};
-  if (warp < kLoadWarps && (int)blockIdx.x < tiles_g * S_g) {
-    const int tg = blockIdx.x / S_g;
-    const int32_t* idp = p.ids_base + (long long)(tg / tps_g) * p.ids_stride + (tg % tps_g) * kBM;
-    const int lim = p.max_ids - (tg % tps_g) * kBM - 1;
-    gid_pre[0] = __ldg(idp + min(lr, lim));
-    gid_pre[1] = __ldg(idp + min(lr + 64, lim));
-  }
-  if (warp == 0) {
-    int t = 0, m0 = 0;
-    for (int b = lane; b < p.batch; b += 32) {
-      const int m = clamp_nact(p, b);
-      if (b == 0) m0 = m;
-      t += (m + kBM - 1) / kBM;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if (lane == 0) {
-      sh_tiles = t;
-      sh_S = (t >= G || t == 0) ? 1 : min(KB, G / t);
-      sh_m0 = m0;
-    }
-  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int tiles = sh_tiles, S = sh_S, units = tiles * S;
-  const bool guess_ok = (S == S_g && tiles == tiles_g);
   constexpr uint32_t idesc = make_idesc(kBM, NT);
+  // Loader pattern: thread t moves 16-B chunk (t & 7) of tile rows lr and
+  // lr + 64 (lr = t >> 3) of every W stage, and of H rows lr + 64 i < NT.
+  const int lr = tid >> 3;
+  const uint32_t swz = (uint32_t)(((tid & 7) ^ (lr & 7)) << 4);
+  uint2* wscratch = reinterpret_cast<uint2*>(smem + C::kPBytes + warp * C::kWarpScratch);
+  const int wcap = C::kWarpScratch / 8;
+  const float* Pm = reinterpret_cast<const float*>(smem);  // partial tile [NT][128] after the MMAs
 
+  const int tiles_g = p.batch * a.tps;
+  const int split = S > 1 ? (int)cluster_ctarank() : 0;
+  const int first = S > 1 ? (int)blockIdx.x / S : (int)blockIdx.x;
+  const int step = S > 1 ? tiles_g : (int)gridDim.x;
   int it = 0;      // pipeline iteration counter across units
   int local = 0;   // units processed by this CTA
-  int seq = 0, seq_tile0 = 0, seq_m = sh_m0;  // tile -> sequence walk (units are tile-major)
-  for (int u = blockIdx.x; u < units; u += G, ++local) {
-    const int tile = u / S, split = u - (u / S) * S;
-    while (tile - seq_tile0 >= (seq_m + kBM - 1) / kBM) {  // advance to the tile's sequence
-      seq_tile0 += (seq_m + kBM - 1) / kBM;
-      ++seq;
-      seq_m = clamp_nact(p, seq);
-    }
-    const int row0 = (tile - seq_tile0) * kBM;
-    const int rows = min(kBM, seq_m - row0);
+  for (int tile = first; tile < tiles_g; tile += step) {
+    const int seq = tile / a.tps, tin = tile - (tile / a.tps) * a.tps;
+    const int m = clamp_nact(p, seq);
+    const int row0 = tin * kBM;
+    const int rows = min(kBM, m - row0);
+    if (rows <= 0) continue;  // the whole cluster (same tile) skips together
+    const int ntiles = (m + kBM - 1) / kBM;
     const int kb0 = split * KB / S, kb1 = (split + 1) * KB / S;
     const int nk = kb1 - kb0;
+    if (tid < kBM) {
+      const int32_t* idp = p.ids_base + (long long)seq * p.ids_stride + row0;
+      ids_s[tid] = __ldg(idp + min(tid, rows - 1));
+    }
+    __syncthreads();
 
     if (warp < kLoadWarps) {
       // ---------------- producers: gather rows of W_head + H into SW128 stages
-      int32_t gid[2];
-      if (local == 0 && guess_ok) {
-        gid[0] = gid_pre[0];
-        gid[1] = gid_pre[1];
-      } else {
-        const int32_t* idp = p.ids_base + (long long)seq * p.ids_stride + row0;
-        gid[0] = __ldg(idp + min(lr, rows - 1));
-        gid[1] = __ldg(idp + min(lr + 64, rows - 1));
-      }
       const uint16_t* rp[2];
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const long long row = p.n_shards > 1 ? gid[i] / p.n_shards : gid[i];
+        const int32_t g = ids_s[lr + 64 * i];
+        const long long row = p.n_shards > 1 ? g / p.n_shards : g;
         rp[i] = (lr + 64 * i < rows) ? p.w + row * p.ldw + (tid & 7) * 8 : nullptr;
       }
       const uint16_t* hp = p.h + (long long)seq * p.n * p.d + (tid & 7) * 8;
@@ -521,14 +495,14 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
         }
       }
       if (tid == 0 && local == 0) trace_mark(p.trace, 3);  // all loads issued and landed
-      // ---------------- epilogue: TMEM -> registers -> partial tile (L2)
+      // ---------------- epilogue: TMEM -> registers -> partial tile P in shared memory
       mbar_wait(smem_u32(&bars[2 * C::kStages]), local & 1);
       tc_fence_after();
       if (tid == 0 && local == 0) trace_mark(p.trace, 4);  // last MMA done
       const int lg = warp & 3, cgp = warp >> 2;   // TMEM lane group, column group
       const int r = lg * 32 + lane;               // TMEM lane == tile row
       const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16);
-      float* dst = a.part + (long long)u * NT * kBM + r;
+      float* Pw = reinterpret_cast<float*>(smem) + r;
       if (cgp < C::kColGroups) {
 #pragma unroll 1
         for (int c0 = cgp * 16; c0 < NT && c0 < p.n; c0 += 16 * C::kColGroups) {
@@ -536,7 +510,7 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
           tmem_ld16(taddr + c0, v);
 #pragma unroll
           for (int c = 0; c < 16; ++c)
-            if (c0 + c < p.n) __stcg(dst + (c0 + c) * kBM, v[c]);
+            if (c0 + c < p.n) Pw[(c0 + c) * kBM] = v[c];
         }
       }
       tc_fence_before();
@@ -563,94 +537,59 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
         }
         __syncwarp();
       }
+      // the MMA warp joins below once the epilogue has drained TMEM
+      mbar_wait(smem_u32(&bars[2 * C::kStages + 1]), local & 1);
     }
     it += nk;
 
-    // ---------------- split-K reduction, distributed over the tile's S CTAs:
-    // once all S partials of the tile are written (per-tile arrival counter;
-    // the launch is cooperative so the spin is safe), split s sums, in split
-    // order, quads [32 s / S, 32 (s+1) / S) of the tile's rows for every node
-    // and writes the final logits.
-    __threadfence();
-    __syncthreads();
-    if (S > 1) {
-      if (tid == 0) {
-        atomicAdd(&a.counters[2 + tile], 1u);
-        while (ld_acquire(&a.counters[2 + tile]) < (unsigned)S) __nanosleep(20);
-      }
-      __syncthreads();
-    }
-    if (tid == 0 && local == 0) trace_mark(p.trace, 5);  // tile's partials complete
-    {
-      const int q0 = split * (kBM / 4) / S, q1 = (split + 1) * (kBM / 4) / S;
-      const int nq = q1 - q0;
-      for (int item = tid; item < p.n * nq; item += kThreads) {
-        const int c = item / nq, r = 4 * (q0 + item - (item / nq) * nq);
-        if (r >= rows) continue;
-        const float* src = a.part + ((long long)tile * S * NT + c) * kBM + r;
-        float4 x[8];
+    // ---------------- split-K reduction over the cluster, level-1 top-k
+    __syncthreads();  // P complete in this CTA
+    if (S > 1) cluster_sync();  // ... and in every CTA of the cluster
+    if (tid == 0 && local == 0) trace_mark(p.trace, 5);  // partials complete
+    if (lane == 0) sh_last[warp] = 0;
+    for (int c = split + S * warp; c < p.n; c += S * kWarps) {
+      // node c, rows 4*lane .. 4*lane+3: sum of the S partials in split order
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      const uint32_t la = smem_u32(Pm + c * kBM + 4 * lane);
+      if (S == 1) {
+        acc = *reinterpret_cast<const float4*>(Pm + c * kBM + 4 * lane);
+      } else {
+        float4 x[kMaxCluster];
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (q < S) x[q] = __ldcg(reinterpret_cast<const float4*>(src + (long long)q * NT * kBM));
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int s2 = 0; s2 < kMaxCluster; ++s2)
+          if (s2 < S) x[s2] = ld_dsmem_v4(mapa_shared(la, (uint32_t)s2));
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (q < S) { acc.x += x[q].x; acc.y += x[q].y; acc.z += x[q].z; acc.w += x[q].w; }
-        for (int q = 8; q < S; ++q) {
-          const float4 y = __ldcg(reinterpret_cast<const float4*>(src + (long long)q * NT * kBM));
-          acc.x += y.x; acc.y += y.y; acc.z += y.z; acc.w += y.w;
-        }
-        float* dst = a.zl + ((long long)seq * p.n + c) * p.max_ids + row0 + r;
-        if (((uintptr_t)dst & 15) == 0 && r + 4 <= rows) {
-          __stcg(reinterpret_cast<float4*>(dst), acc);
-        } else {
-          const float vv[4] = {acc.x, acc.y, acc.z, acc.w};
-          for (int i = 0; i < 4 && r + i < rows; ++i) __stcg(dst + i, vv[i]);
-        }
+        for (int s2 = 0; s2 < kMaxCluster; ++s2)
+          if (s2 < S) { acc.x += x[s2].x; acc.y += x[s2].y; acc.z += x[s2].z; acc.w += x[s2].w; }
       }
-    }
-  }
-
-  // ---------------- grid barrier: every logit reduced
-  if (tid == 0) trace_mark(p.trace, 6);  // reduction done
-  __threadfence();
-  tc_fence_before();
-  __syncthreads();
-  const int tasks = p.batch * p.n;
-  if (tid == 0) {
-    atomicAdd(&a.counters[0], 1u);
-    if ((int)blockIdx.x < tasks)  // CTAs with top-k work wait for everyone
-      while (ld_acquire(&a.counters[0]) < (unsigned)G) __nanosleep(32);
-    trace_mark(p.trace, 12);  // grid barrier passed
-  }
-  __syncthreads();
-
-  // ---------------- top-k: (sequence, node) tasks over the CTAs
-  {
-    int tseq = 0, tm = sh_m0;
-    for (int t = blockIdx.x; t < tasks; t += G) {
-      const int sq = t / p.n, node = t - (t / p.n) * p.n;
-      while (tseq < sq) {
-        ++tseq;
-        tm = clamp_nact(p, tseq);
+      const float v[4] = {acc.x, acc.y, acc.z, acc.w};
+      const int32_t g[4] = {ids_s[4 * lane], ids_s[4 * lane + 1], ids_s[4 * lane + 2], ids_s[4 * lane + 3]};
+      if (p.logits) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (4 * lane + i < rows) p.logits[((long long)seq * p.n + c) * p.max_ids + row0 + 4 * lane + i] = v[i];
       }
-      topk_node<NT>(a, sq, node, tm, smem, tsh);
+      uint2* cout = a.cand + ((long long)tile * p.n + c) * a.k;
+      level1(v, g, 4 * lane, rows, a.k, wscratch, cout, &a.tstat[(long long)tile * p.n + c]);
+      // level 2: the warp whose list completes the node merges it.  The warp's
+      // list is published by lane 0's release (after the warp barrier); the
+      // last arriver's acquire makes every tile's list visible.
+      __syncwarp();
+      unsigned last = 0;
+      if (lane == 0) {
+        last = atom_add_acq_rel(&a.node_ctr[seq * p.n + c], 1u) == (unsigned)(ntiles - 1);
+        if (last) a.node_ctr[seq * p.n + c] = 0u;  // every other tile has arrived: reset for the next launch
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) level2(a, seq, c, seq * a.tps, ntiles, wscratch, wcap);
     }
+    if (tid == 0 && local == 0) trace_mark(p.trace, 6);  // level 1 (+ merges) done
+    if (S > 1) cluster_sync();  // peers are done reading this CTA's partials
+    __syncthreads();            // P / scratch free for the next unit
+    ++local;
   }
 
-  // ---------------- teardown: last CTA out resets the counters for the next launch
-  if (tid == 0) trace_mark(p.trace, 8);  // top-k done
-  __syncthreads();
-  if (tid == 0) {
-    const unsigned old = atomicAdd(&a.counters[1], 1u);
-    sh_tiles = (old == (unsigned)G - 1) ? 1 : 0;
-  }
-  __syncthreads();
-  if (sh_tiles) {  // the last CTA: every other CTA has passed all its waits
-    for (int t = tid; t < tiles; t += kThreads) a.counters[2 + t] = 0u;
-    if (tid == 0) { a.counters[0] = 0u; a.counters[1] = 0u; }
-    __threadfence();
-  }
+  if (tid == 0) trace_mark(p.trace, 8);  // done
   tc_fence_before();
   __syncthreads();
   if (warp == kLoadWarps) {
@@ -660,23 +599,20 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
 }
 
 struct ScratchLayout {
-  size_t counters, part, zl, total;
+  size_t node_ctr, cand, tstat, total;
 };
 
-inline ScratchLayout scratch_layout(int batch, int max_ids, int n, int nt) {
-  const size_t max_tiles = (size_t)batch * ((max_ids + kBM - 1) / kBM);
-  const size_t units_cap = max_tiles > (size_t)kMaxSMs ? max_tiles : (size_t)kMaxSMs;
+inline ScratchLayout scratch_layout(int batch, int max_ids, int n) {
+  const size_t tiles = (size_t)batch * ((max_ids + kBM - 1) / kBM);
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
   ScratchLayout L;
   size_t off = 0;
-  L.counters = off; off += al(sizeof(unsigned) * (2 + max_tiles));
-  L.part = off;     off += al(units_cap * nt * kBM * sizeof(float));
-  L.zl = off;       off += al((size_t)batch * n * max_ids * sizeof(float));
+  L.node_ctr = off; off += al(sizeof(unsigned) * (size_t)batch * n);
+  L.cand = off;     off += al(tiles * (size_t)n * kMaxK * sizeof(uint2));
+  L.tstat = off;    off += al(tiles * (size_t)n * sizeof(float2));
   L.total = off;
   return L;
 }
-
-inline int nt_for(int n) { return n <= 16 ? 16 : n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : 256; }
 
 template <int NT>
 cudaError_t launch_nt(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse, void* scratch,
@@ -689,37 +625,77 @@ cudaError_t launch_nt(const HeadProblem& p, int k, float* topk_logit, int32_t* t
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int grid = num_sms < kMaxSMs ? num_sms : kMaxSMs;
-  const ScratchLayout L = scratch_layout(p.batch, p.max_ids, p.n, NT);
+  const ScratchLayout L = scratch_layout(p.batch, p.max_ids, p.n);
   if (L.total > scratch_bytes) return cudaErrorInvalidValue;
   char* sc = (char*)scratch;
   TcArgs a;
   a.p = p;
-  a.counters = (unsigned*)(sc + L.counters);
-  a.part = (float*)(sc + L.part);
-  a.zl = p.logits ? p.logits : (float*)(sc + L.zl);
+  a.node_ctr = (unsigned*)(sc + L.node_ctr);
+  a.cand = (uint2*)(sc + L.cand);
+  a.tstat = (float2*)(sc + L.tstat);
   a.topk_logit = topk_logit;
   a.topk_id = topk_id;
   a.lse = lse;
   a.k = k;
-  a.max_tiles = p.batch * ((p.max_ids + kBM - 1) / kBM);
+  a.tps = (p.max_ids + kBM - 1) / kBM;
+  const int G = num_sms < kMaxSMs ? num_sms : kMaxSMs;
+  const int tiles_g = p.batch * a.tps;
+  const int KB = p.d / kBK;
+  // Largest cluster (K-split) size S <= 8 whose tiles_g clusters are all
+  // co-resident in one wave (GPC packing decides, so ask the runtime; cached).
+  static int max_clusters[kMaxCluster + 1] = {0};
+  int S = 1;
+  if (tiles_g < G) {
+    for (int s = kMaxCluster; s >= 2; --s) {
+      if (s > KB || s * tiles_g > G) continue;
+      if (max_clusters[s] == 0) {
+        cudaLaunchConfig_t q = {};
+        q.gridDim = dim3(s * tiles_g);
+        q.blockDim = dim3(kThreads);
+        q.dynamicSmemBytes = C::kSmemBytes;
+        cudaLaunchAttribute ca;
+        ca.id = cudaLaunchAttributeClusterDimension;
+        ca.val.clusterDim.x = s;
+        ca.val.clusterDim.y = 1;
+        ca.val.clusterDim.z = 1;
+        q.attrs = &ca;
+        q.numAttrs = 1;
+        int nc = 0;
+        if (cudaOccupancyMaxActiveClusters(&nc, head_tc_kernel<NT>, &q) != cudaSuccess || nc <= 0) {
+          (void)cudaGetLastError();
+          nc = -1;
+        }
+        max_clusters[s] = nc;
+      }
+      if (max_clusters[s] >= tiles_g) { S = s; break; }
+    }
+  }
+  a.S = S;
 
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
+  cfg.gridDim = dim3(S > 1 ? tiles_g * S : (tiles_g < G ? tiles_g : G));
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = C::kSmemBytes;
   cfg.stream = stream;
   cudaLaunchAttribute attrs[2];
-  attrs[0].id = cudaLaunchAttributeCooperative;
-  attrs[0].val.cooperative = 1;
-  attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attrs[1].val.programmaticStreamSerializationAllowed = 1;
+  int na = 0;
+  attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[na].val.programmaticStreamSerializationAllowed = 1;
+  ++na;
+  if (S > 1) {
+    attrs[na].id = cudaLaunchAttributeClusterDimension;
+    attrs[na].val.clusterDim.x = S;
+    attrs[na].val.clusterDim.y = 1;
+    attrs[na].val.clusterDim.z = 1;
+    ++na;
+  }
   cfg.attrs = attrs;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = na;
   cudaError_t e = cudaLaunchKernelEx(&cfg, head_tc_kernel<NT>, a);
   if (e != cudaSuccess) {
     (void)cudaGetLastError();
-    cfg.numAttrs = 1;  // cooperative only
+    cfg.attrs = attrs + 1;  // without PDL
+    cfg.numAttrs = na - 1;
     e = cudaLaunchKernelEx(&cfg, head_tc_kernel<NT>, a);
   }
   return e;
@@ -727,9 +703,7 @@ cudaError_t launch_nt(const HeadProblem& p, int k, float* topk_logit, int32_t* t
 
 }  // namespace
 
-size_t head_tc_scratch_bytes(int batch, int max_ids, int n) {
-  return scratch_layout(batch, max_ids, n, nt_for(n)).total;
-}
+size_t head_tc_scratch_bytes(int batch, int max_ids, int n) { return scratch_layout(batch, max_ids, n).total; }
 
 cudaError_t launch_head_tc(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse,
                            void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t stream) {

@@ -15,8 +15,8 @@ import paper_2605_26444_b200 as P  # noqa: E402
 from paper_2605_26444_b200 import _native as N  # noqa: E402
 from synthetic import inputs as SI  # noqa: E402
 
-EVENTS = ["start", "dep_ok", "rowptr", "loads_landed", "mma_done", "tile_ready", "reduced", "tk_gathered",
-          "topk_done", "tk_thresh", "tk_compacted", "tk_ranked", "grid_bar"]
+EVENTS = ["start", "dep_ok", "rowptr", "loads_landed", "mma_done", "partials_ready", "level1_done", "-",
+          "done"]
 
 
 def main():
