@@ -386,7 +386,7 @@ def run_ours(args):
         us_cpu, sample = cpu_oracle_steps(cfg, n, k, args.cpu_sample_steps)
         cpu = {"value": round(us_cpu, 1), "unit": "us/step", "cores": 1, "kind": "oracle", "sample": sample}
 
-    launches_per_step = 3  # state update + head contraction + top-k select
+    launches_per_step = 3 if args.head == "simt" else 2  # state update + fused head (SIMT: + select)
     value = ms_total * 1e3 / (K * world)
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "us/step", "n_gpus": world, "steps": K,

@@ -14,26 +14,28 @@
 // padded), K = 64 per pipeline stage; D in TMEM (NT fp32 columns).  A launch
 // covers tiles_g = batch * ceil(max_ids / 128) row tiles (tiles past a
 // sequence's n_active, read from device memory, exit at once).  With
-// tiles_g < #SMs every tile is split along K into S = min(8, #SMs / tiles_g)
-// chunks handled by the S CTAs of one thread-block cluster, so ~all SMs stream.
+// tiles_g < #SMs every tile is split along K into S = #SMs / tiles_g chunks
+// (S = 6 at |I| = 3072: 144 CTAs stream), one CTA per (tile, chunk); with
+// tiles_g >= #SMs (e.g. the dense [0, V) comparator) S = 1 and persistent CTAs
+// loop over tiles.
 //
-// Reduction + top-k, no grid-wide synchronisation:
-//  1. each CTA drains its partial tile from TMEM into its own shared memory;
-//     after a cluster barrier, CTA s sums -- over distributed shared memory, in
-//     split order (fixed order: equal rows give bit-equal logits) -- the 128
-//     rows of nodes s, s+S, ...;
-//  2. level 1, one warp per (tile, node): exact top-k of the 128 logits
-//     (threshold = k-th largest lane maximum, compaction, rank by counting)
-//     and (max, sum exp) for the lse, written to L2-resident scratch;
-//  3. level 2: a per-(sequence, node) arrival counter; the warp that brings it
-//     to ceil(n_active / 128) merges that node's sorted per-tile lists
-//     (threshold = k-th largest list head, rank by counting) and combines the
-//     lse partials -- the last arriver finishes the node, nobody waits.
+// Reduction + top-k: every CTA drains its partial tile from TMEM straight to
+// an L2-resident buffer P[tile][split][node][128] and arrives at a one-word
+// grid counter (arrivals in the low bits; the last arriver bumps a generation
+// field).  CTAs 0 .. batch*n-1 are the finishers of the (sequence, node) pairs:
+// they wait for the generation to change, sum the S partials of every active
+// row in split order (fixed order: equal rows give bit-equal logits), keep the
+// online (max, sum exp) for lse, and select the top-k in registers (per-thread
+// sorting network, then k rounds of a warp arg-max by two redux instructions,
+// then a merge of the per-warp lists).  The other CTAs leave as soon as they
+// have arrived.  All CTAs of a launch are co-resident (grid <= #SMs, one CTA
+// per SM), so the finishers' wait cannot deadlock.
 //
 // Warp roles (544 threads): warps 0-15 load (cp.async) and drain TMEM (warp w
 // reads TMEM lanes 32*(w%4).. and a quarter of the columns); warp 16 allocates
 // TMEM and one lane issues the MMAs.  All 17 warps run the reduction / top-k.
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "internal.h"
@@ -51,19 +53,35 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kSmemBudget = 192 * 1024;
 constexpr int kMaxSMs = 256;
 constexpr int kMaxK = 32;
-constexpr int kMaxCluster = 8;    // portable cluster size
-constexpr int kL2Tiles = 64;      // tiles per sequence whose level-2 inputs are fetched in one round trip
+constexpr int kMaxSplit = 32;     // K splits per tile
+constexpr int kFinRows = 8;       // rows per finisher thread per round
+constexpr int kCountBits = 12;    // grid barrier word: arrivals in bits [0, 12), generation above
+// Poll mode hands data between CTAs without fences or flags: every 32-bit word
+// is stored XOR-ed with a constant that no real value equals, so a word reads
+// as 0 exactly until its producer's store has landed; the consumer re-zeroes
+// what it consumed (the scratch starts zeroed, ABI).
+constexpr uint32_t kEncF = 0x7fbadbadu;  // partial logits / lse floats: a NaN payload arithmetic never makes
+constexpr uint32_t kEncK = 0x00000001u;  // list keys: float_key(v) == 1 only for NaN bit patterns
+constexpr uint32_t kEncG = 0x7fffffffu;  // list ids: valid ids are < 2^31 - 1, padding is 0xffffffff
+constexpr int kModeFinish = 0;   // persistent CTAs, grid barrier, one finisher CTA per (sequence, node)
+constexpr int kModePoll = 1;     // one unit per CTA, split-K partials + lists handed over through L2
+constexpr int kModeCluster = 2;  // one unit per CTA, the S splits of a tile form a cluster (DSMEM reduction)
+constexpr int kMaxCluster = 8;   // portable cluster size
+constexpr int kMaxL2Lists = 160;  // poll mode: tiles per sequence (5 lists per lane at level 2)
+constexpr long long kSpinLimit = 1ll << 26;  // polls before giving up (a trap beats a hung GPU)
 
 struct TcArgs {
   HeadProblem p;
-  uint2* cand;          // [tiles_g][n][k] level-1 lists (float_key, global id), best first
-  float2* tstat;        // [tiles_g][n] (max, sum exp(z - max)) over a tile's rows
-  unsigned* node_ctr;   // [batch * n] level-1 arrivals per (sequence, node); zero between launches
+  unsigned* grid_word;  // grid barrier: (generation << kCountBits) | arrivals
+  float* part;          // [tiles_g * S][n][128] partial tiles (split-K partials, or whole tiles for S = 1)
+  uint2* cand;          // poll mode: [tiles_g][n][k + 1] level-1 lists (+ lse partial), encoded
+  int mode;             // kModeCluster / kModePoll / kModeFinish (see the launcher)
+  unsigned* node_ctr;   // cluster mode: [batch * n] level-1 arrivals per (sequence, node); zero between launches
   float* topk_logit;    // [batch][n][k]
   int32_t* topk_id;
   float* lse;           // [batch][n] or null
   int k;
-  int S;                // K splits per tile == cluster size (1: no cluster, persistent CTAs)
+  int S;                // K splits per tile (1: persistent CTAs loop over tiles)
   int tps;              // tiles per sequence = ceil(max_ids / 128)
 };
 
@@ -147,6 +165,23 @@ __device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
   return old;
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ uint4 ld_relaxed_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint2 ld_relaxed_v2(const void* p) {
+  uint2 v;
+  asm volatile("ld.relaxed.gpu.global.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_f32(float* p, float v) {
+  asm volatile("st.relaxed.gpu.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_v2(uint2* p, uint2 v) {
+  asm volatile("st.relaxed.gpu.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
+}
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -169,6 +204,10 @@ __device__ __forceinline__ float4 ld_dsmem_v4(uint32_t caddr) {
                : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v);
+__device__ __forceinline__ void red_add_release(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ int clamp_nact(const HeadProblem& p, int b) {
   int m = p.nact_base[(long long)b * p.nact_stride];
   return m < 0 ? 0 : (m > p.max_ids ? p.max_ids : m);
@@ -182,13 +221,9 @@ struct Cfg {
   static constexpr int kStages = (kSmemBudget / kStageBytes) > 8 ? 8 : (kSmemBudget / kStageBytes);
   static constexpr int kTmemCols = NT < 32 ? 32 : NT;
   static constexpr int kStageArea = kStages * kStageBytes;
-  // after the MMAs the stage area holds the partial tile P[NT][128] fp32 and a
-  // per-warp scratch for the selections
-  static constexpr int kPBytes = NT * kBM * 4;
-  static constexpr int kWarpScratch = ((kStageArea - kPBytes) / kWarps) / 8 * 8;  // bytes
-  static_assert(kWarpScratch >= kBM * 8, "per-warp scratch");
   static constexpr int kSmemBytes = kStageArea + 1024 /*align*/ + 256 /*barriers*/;
   static_assert(2 * kStages + 3 <= 30, "barrier area");
+  static_assert(kWarps * kMaxK * 8 + kWarps * 8 + kMaxSplit * kBM * 4 + 1024 <= kStageArea, "finisher scratch");
   static constexpr int kHChunks = NT * 8;                 // 16-B chunks of one H stage
   static constexpr int kColGroups = NT / 16 < 4 ? NT / 16 : 4;  // epilogue column groups
 };
@@ -198,9 +233,169 @@ __device__ __forceinline__ float key_value(uint32_t kk) {
   return __uint_as_float((kk & 0x80000000u) ? (kk & 0x7fffffffu) : ~kk);
 }
 // (value desc, id asc): a before b
-__device__ __forceinline__ bool key_before(uint32_t ka, int32_t ga, uint32_t kb, int32_t gb) {
+__device__ __forceinline__ bool key_before(uint32_t ka, uint32_t ga, uint32_t kb, uint32_t gb) {
   return ka > kb || (ka == kb && ga < gb);
 }
+// Compare-exchange: afterwards entry a precedes entry b in (value desc, id asc).
+__device__ __forceinline__ void cx(uint32_t& ka, uint32_t& ga, uint32_t& kb, uint32_t& gb) {
+  if (key_before(kb, gb, ka, ga)) {
+    const uint32_t tk = ka; ka = kb; kb = tk;
+    const uint32_t tg = ga; ga = gb; gb = tg;
+  }
+}
+// Sort 8 entries (19-comparator network).
+__device__ __forceinline__ void sort8(uint32_t (&k)[kFinRows], uint32_t (&g)[kFinRows]) {
+#define NS_CX(i, j) cx(k[i], g[i], k[j], g[j])
+  NS_CX(0, 2); NS_CX(1, 3); NS_CX(4, 6); NS_CX(5, 7);
+  NS_CX(0, 4); NS_CX(1, 5); NS_CX(2, 6); NS_CX(3, 7);
+  NS_CX(0, 1); NS_CX(2, 3); NS_CX(4, 5); NS_CX(6, 7);
+  NS_CX(2, 4); NS_CX(3, 5);
+  NS_CX(1, 4); NS_CX(3, 6);
+  NS_CX(1, 2); NS_CX(3, 4); NS_CX(5, 6);
+#undef NS_CX
+}
+// k rounds of a warp arg-max over the heads of per-lane sorted lists of L
+// entries (key 0 = none): round r's winner goes to lane r, the winning lane
+// shifts its list.  Returns this lane's entry of the warp's sorted top-k.
+template <int L>
+__device__ __forceinline__ uint2 warp_select(uint32_t (&k)[L], uint32_t (&g)[L], int kk) {
+  const int lane = threadIdx.x & 31;
+  uint2 mine = make_uint2(0u, 0xffffffffu);
+  for (int r = 0; r < kk; ++r) {
+    const uint32_t wk = __reduce_max_sync(0xffffffffu, k[0]);
+    if (wk == 0u) break;  // fewer than kk entries: the rest stays padding
+    const unsigned tied = __ballot_sync(0xffffffffu, k[0] == wk);
+    // one holder of the maximum (the usual case): its id; a tie: the smallest id
+    const uint32_t wg = (tied & (tied - 1u)) ? __reduce_min_sync(0xffffffffu, k[0] == wk ? g[0] : 0xffffffffu)
+                                             : __shfl_sync(0xffffffffu, g[0], __ffs(tied) - 1);
+    if (lane == r) mine = make_uint2(wk, wg);
+    if (k[0] == wk && g[0] == wg) {
+#pragma unroll
+      for (int i = 0; i + 1 < L; ++i) { k[i] = k[i + 1]; g[i] = g[i + 1]; }
+      k[L - 1] = 0u;
+    }
+  }
+  return mine;
+}
+// Online lse partial: fold (m2, e2) into (m, e), e = sum exp(z - m).
+__device__ __forceinline__ void lse_fold(float& m, float& e, float m2, float e2) {
+  if (m2 == -INFINITY) return;
+  if (m == -INFINITY) { m = m2; e = e2; return; }
+  if (m2 > m) { e = e * __expf(m - m2) + e2; m = m2; }
+  else e += e2 * __expf(m2 - m);
+}
+
+// Finisher of one (sequence, node): logits of the m active rows = sum of the S
+// partials in split order; top-k by (value desc, id asc) mapped to global ids;
+// lse over the active set.  Rows go in rounds of `rr` (a multiple of
+// 128, <= kThreads * kFinRows): the round's S partial slices are staged in
+// shared memory `sp` by 16-byte cp.async (one round trip, no registers held),
+// then thread t sums rows t, t + kThreads, ...  `wl` holds kWarps lists of k
+// entries, `wm` kWarps (max, sum exp) pairs.
+__device__ void finish_node(const TcArgs& a, int seq, int node, float* sp, int rr, uint2* wl, float2* wm) {
+  const HeadProblem& p = a.p;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int k = a.k, S = a.S;
+  const int m = clamp_nact(p, seq);
+  const int32_t* ids = p.ids_base + (long long)seq * p.ids_stride;
+  const long long pstride = (long long)p.n * kBM;  // floats between consecutive (tile, split) slots
+  const float* pbase = a.part + (long long)seq * a.tps * S * pstride + (long long)node * kBM;
+  float tm = -INFINITY, te = 0.f;  // this thread's lse partial
+  uint2 run = make_uint2(0u, 0xffffffffu);  // this lane's entry of the warp's running top-k
+  for (int r0 = 0; r0 < m; r0 += rr) {
+    const int nrow = min(rr, m - r0);
+    const int ntl = (nrow + kBM - 1) / kBM;  // tiles of this round
+    const int nchunks = S * ntl * (kBM / 4);  // 16-B chunks: (split, tile, quarter-row group)
+    for (int c = tid; c < nchunks; c += kThreads) {
+      const int q = c & (kBM / 4 - 1), tl = (c / (kBM / 4)) % ntl, sidx = c / (kBM / 4 * ntl);
+      const float* src = pbase + ((long long)(r0 / kBM + tl) * S + sidx) * pstride + q * 4;
+      cp_async16(smem_u32(sp + (long long)sidx * rr + tl * kBM + q * 4), src, 16u);
+    }
+    cp_async_commit();
+    uint32_t key[kFinRows], gid[kFinRows];
+#pragma unroll
+    for (int i = 0; i < kFinRows; ++i) {
+      const int j = i * kThreads + tid;
+      gid[i] = j < nrow ? (uint32_t)__ldcg(ids + r0 + j) : 0xffffffffu;
+    }
+    cp_async_wait<0>();
+    for (int c = tid; c < nchunks; c += kThreads) {  // leave the scratch zeroed for poll-mode launches
+      const int q = c & (kBM / 4 - 1), tl = (c / (kBM / 4)) % ntl, sidx = c / (kBM / 4 * ntl);
+      float* src = const_cast<float*>(pbase) + ((long long)(r0 / kBM + tl) * S + sidx) * pstride + q * 4;
+      *reinterpret_cast<uint4*>(src) = make_uint4(0u, 0u, 0u, 0u);
+    }
+    __syncthreads();
+    if (tid == 0 && r0 == 0 && (int)blockIdx.x == seq * p.n + node) trace_mark(p.trace, 10);  // partials staged
+#pragma unroll
+    for (int i = 0; i < kFinRows; ++i) {
+      const int j = i * kThreads + tid;
+      key[i] = 0u;
+      if (j < nrow) {
+        float z = 0.f;
+        for (int s2 = 0; s2 < S; ++s2) z += sp[s2 * rr + j];
+        key[i] = float_key(z);
+        lse_fold(tm, te, z, 1.f);
+        if (p.logits) p.logits[((long long)seq * p.n + node) * p.max_ids + r0 + j] = z;
+      }
+    }
+    __syncthreads();  // sp free for the next round
+    if (tid == 0 && r0 == 0 && (int)blockIdx.x == seq * p.n + node) trace_mark(p.trace, 11);  // summed
+    sort8(key, gid);
+    const uint2 c = warp_select<kFinRows>(key, gid, k);
+    if (tid == 0 && r0 == 0 && (int)blockIdx.x == seq * p.n + node) trace_mark(p.trace, 12);  // warp top-k
+    if (r0 == 0) {
+      run = c;
+    } else {  // merge the round's list into the running one (two sorted entries per lane)
+      uint32_t mk[2] = {run.x, c.x}, mg[2] = {run.y, c.y};
+      cx(mk[0], mg[0], mk[1], mg[1]);
+      run = warp_select<2>(mk, mg, k);
+    }
+  }
+  // lse: warp, then block
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, tm, o), e2 = __shfl_xor_sync(0xffffffffu, te, o);
+    lse_fold(tm, te, m2, e2);
+  }
+  if (lane < k) wl[warp * k + lane] = run;
+  if (lane == 0) wm[warp] = make_float2(tm, te);
+  __syncthreads();
+  if (tid == 0 && (int)blockIdx.x == seq * p.n + node) trace_mark(p.trace, 13);  // lists in smem
+  if (warp == 0) {
+    // merge the kWarps sorted lists: lane t holds list t's head
+    int hp = 0;
+    uint32_t hk[1], hg[1];
+    hk[0] = lane < kWarps ? wl[lane * k].x : 0u;
+    hg[0] = lane < kWarps ? wl[lane * k].y : 0xffffffffu;
+    uint2 mine = make_uint2(0u, 0xffffffffu);
+    for (int r = 0; r < k; ++r) {
+      const uint32_t wk = __reduce_max_sync(0xffffffffu, hk[0]);
+      if (wk == 0u) break;
+      const uint32_t wg = __reduce_min_sync(0xffffffffu, hk[0] == wk ? hg[0] : 0xffffffffu);
+      if (lane == r) mine = make_uint2(wk, wg);
+      if (hk[0] == wk && hg[0] == wg) {
+        ++hp;
+        const uint2 nx = hp < k ? wl[lane * k + hp] : make_uint2(0u, 0xffffffffu);
+        hk[0] = nx.x; hg[0] = nx.y;
+      }
+    }
+    float bm = -INFINITY, be = 0.f;
+    if (lane < kWarps) { bm = wm[lane].x; be = wm[lane].y; }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, bm, o), e2 = __shfl_xor_sync(0xffffffffu, be, o);
+      lse_fold(bm, be, m2, e2);
+    }
+    const long long ob = ((long long)seq * p.n + node) * k;
+    if (lane < k) {
+      a.topk_logit[ob + lane] = mine.x ? key_value(mine.x) : -INFINITY;
+      a.topk_id[ob + lane] = mine.x ? (int32_t)mine.y : -1;
+    }
+    if (a.lse && lane == 0) a.lse[(long long)seq * p.n + node] = bm == -INFINITY ? -INFINITY : bm + logf(be);
+  }
+  __syncthreads();  // wl / wm free for the next pair
+}
+
 // k-th largest (1 <= k <= 32) of one key per lane, by counting (ties by lane).
 __device__ __forceinline__ uint32_t warp_kth_key(uint32_t x, int k) {
   const int lane = threadIdx.x & 31;
@@ -213,9 +408,8 @@ __device__ __forceinline__ uint32_t warp_kth_key(uint32_t x, int k) {
   const unsigned sel = __ballot_sync(0xffffffffu, rank == k - 1);
   return __shfl_sync(0xffffffffu, x, __ffs(sel) - 1);
 }
-
-// Rank `cnt` staged (key, gid) candidates by counting and write the k best
-// (best first) to out[0..k); the warp-private scratch holds the candidates.
+// Rank `cnt` staged (key, gid) candidates by counting (all loads independent)
+// and write the k best, best first, to out[0..k).
 __device__ __forceinline__ void warp_rank_write(const uint2* cs, int cnt, int k, uint2* out) {
   const int lane = threadIdx.x & 31;
   for (int e = lane; e < cnt; e += 32) {
@@ -223,166 +417,343 @@ __device__ __forceinline__ void warp_rank_write(const uint2* cs, int cnt, int k,
     int r = 0;
     for (int f = 0; f < cnt; ++f) {
       const uint2 o = cs[f];
-      r += key_before(o.x, (int32_t)o.y, me.x, (int32_t)me.y) ? 1 : 0;
+      r += key_before(o.x, o.y, me.x, me.y) ? 1 : 0;
     }
     if (r < k) out[r] = me;
   }
 }
-
-// Level 1 for one (tile, node): the 128 logits of the tile's rows (4 per lane).
-// Writes the tile's sorted top-k (key, gid) -- padded with (0, -1) -- and
-// (max, sum exp) of the valid rows.
-__device__ __forceinline__ void level1(const float (&v)[4], const int32_t (&g)[4], int r0, int rows, int k,
-                                       uint2* scratch, uint2* cand_out, float2* tstat_out) {
+// Threshold selection of a warp's top-k from 4 entries per lane (unsorted):
+// T = k-th largest lane maximum (k lanes each own an entry >= T, so every
+// top-k entry is >= T); the entries >= T are compacted into `scratch` and
+// ranked by counting.  Returns this lane's entry of the sorted top-k.
+__device__ __forceinline__ uint2 warp_topk_thr(const uint32_t (&key)[4], const uint32_t (&gid)[4], int k,
+                                               uint2* scratch) {
   const int lane = threadIdx.x & 31;
-  uint32_t key[4];
   uint32_t lmk = 0u;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    key[i] = (r0 + i < rows) ? float_key(v[i]) : 0u;
-    lmk = key[i] > lmk ? key[i] : lmk;
-  }
-  // lse partial
-  const float M = key_value(__reduce_max_sync(0xffffffffu, lmk));
-  float es = 0.f;
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-    if (key[i]) es += __expf(v[i] - M);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
-  // threshold: k-th largest lane maximum (k lanes each own a value >= T)
+  for (int i = 0; i < 4; ++i) lmk = key[i] > lmk ? key[i] : lmk;
   const uint32_t T = warp_kth_key(lmk, k);
   int cnt = 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const bool c = key[i] != 0u && key[i] >= T;
     const unsigned bal = __ballot_sync(0xffffffffu, c);
-    if (c) scratch[cnt + __popc(bal & ((1u << lane) - 1u))] = make_uint2(key[i], (uint32_t)g[i]);
+    if (c) scratch[cnt + __popc(bal & ((1u << lane) - 1u))] = make_uint2(key[i], gid[i]);
     cnt += __popc(bal);
   }
+  uint2* best = scratch + kBM;
+  if (lane < k) best[lane] = make_uint2(0u, 0xffffffffu);
   __syncwarp();
-  if (lane < k) cand_out[lane] = make_uint2(0u, 0xffffffffu);  // padding when rows < k
+  warp_rank_write(scratch, cnt, k, best);
   __syncwarp();
-  warp_rank_write(scratch, cnt, k, cand_out);
-  if (lane == 0) *tstat_out = make_float2(M, es);
+  const uint2 r = lane < k ? best[lane] : make_uint2(0u, 0xffffffffu);
+  __syncwarp();
+  return r;
 }
 
-// Level 2 for one (sequence, node), one warp: merge ntiles sorted lists.
-__device__ void level2(const TcArgs& a, int seq, int node, int tile0, int ntiles, uint2* scratch, int cap) {
+// ---------------------------------------------------------------- poll mode
+// Level 1 for one (tile, node), one warp: wait for the S encoded partials of
+// the node's 128 rows (4 per lane), sum them in split order, zero them, then
+// the tile's sorted top-k (sort 4 per lane, k rounds of a warp arg-max) and
+// (max, sum exp); publishes k encoded (key, id) entries + the lse partial.
+// Cluster mode: the partials are the S cluster CTAs' shared-memory tiles
+// Pm[node][128] (read over DSMEM); the list is published with plain stores
+// (the caller's release atomic orders them).
+template <bool kPollMode>
+__device__ void level1(const TcArgs& a, int tile, int node, const int32_t* ids_s, int rows, int row0,
+                       const float* Pm, uint2* scratch) {
+  const HeadProblem& p = a.p;
+  const int lane = threadIdx.x & 31;
+  const int S = a.S, k = a.k;
+  const long long sstride = (long long)p.n * kBM;  // floats between splits
+  float* src = a.part + ((long long)tile * S * p.n + node) * kBM + 4 * lane;
+  float v[4] = {0.f, 0.f, 0.f, 0.f};
+  if (!kPollMode) {
+    const uint32_t la = smem_u32(Pm + node * kBM + 4 * lane);
+    for (int j0 = 0; j0 < S; j0 += 4) {
+      float4 x[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j0 + j < S) x[j] = ld_dsmem_v4(mapa_shared(la, (uint32_t)(j0 + j)));
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j0 + j < S) { v[0] += x[j].x; v[1] += x[j].y; v[2] += x[j].z; v[3] += x[j].w; }  // split order
+    }
+  }
+  for (int s0 = 0; kPollMode && s0 < S; s0 += 8) {
+    uint4 x[8];
+    long long spins = 0;
+    while (true) {
+      bool ok = true;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (s0 + j < S) {
+          x[j] = ld_relaxed_v4(src + (s0 + j) * sstride);
+          ok = ok && x[j].x && x[j].y && x[j].z && x[j].w;
+        }
+      if (__all_sync(0xffffffffu, ok)) break;
+      if (++spins > kSpinLimit) __trap();
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (s0 + j < S) {  // split order
+        v[0] += __uint_as_float(x[j].x ^ kEncF);
+        v[1] += __uint_as_float(x[j].y ^ kEncF);
+        v[2] += __uint_as_float(x[j].z ^ kEncF);
+        v[3] += __uint_as_float(x[j].w ^ kEncF);
+        *reinterpret_cast<uint4*>(src + (s0 + j) * sstride) = make_uint4(0u, 0u, 0u, 0u);
+      }
+  }
+  const int r0 = 4 * lane;
+  uint32_t key[4], gid[4];
+  float mloc = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool ok = r0 + i < rows;
+    key[i] = ok ? float_key(v[i]) : 0u;
+    gid[i] = ok ? (uint32_t)ids_s[r0 + i] : 0xffffffffu;
+    if (ok) mloc = fmaxf(mloc, v[i]);
+    if (ok && p.logits) {
+      const int seq = tile / a.tps;
+      p.logits[((long long)seq * p.n + node) * p.max_ids + row0 + r0 + i] = v[i];
+    }
+  }
+  // lse partial of the tile's valid rows
+  float M = mloc;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  float es = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (key[i]) es += __expf(v[i] - M);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
+  uint2 mine;
+  if (kPollMode) {
+    cx(key[0], gid[0], key[1], gid[1]);
+    cx(key[2], gid[2], key[3], gid[3]);
+    cx(key[0], gid[0], key[2], gid[2]);
+    cx(key[1], gid[1], key[3], gid[3]);
+    cx(key[1], gid[1], key[2], gid[2]);
+    mine = warp_select<4>(key, gid, k);
+  } else {
+    mine = warp_topk_thr(key, gid, k, scratch);
+  }
+  uint2* out = a.cand + ((long long)tile * p.n + node) * (k + 1);
+  if (kPollMode) {
+    if (lane < k) st_relaxed_v2(out + lane, make_uint2(mine.x ^ kEncK, mine.y ^ kEncG));
+    if (lane == 0) st_relaxed_v2(out + k, make_uint2(__float_as_uint(M) ^ kEncF, __float_as_uint(es) ^ kEncF));
+  } else {
+    if (lane < k) out[lane] = mine;
+    if (lane == 0) out[k] = make_uint2(__float_as_uint(M), __float_as_uint(es));
+  }
+}
+
+// Level 2 for one (sequence, node), one warp: wait for the ntiles encoded
+// lists, stage them (decoded) in the warp's shared scratch, zero them, merge by
+// k rounds of a warp arg-max over the list heads (lane t owns lists t, t+32,
+// ...), combine the lse partials, write the outputs.
+// Cluster mode: the lists are complete (acquired by the caller): plain loads.
+template <int kPer, bool kPollMode>  // lists per lane (ntiles <= 32 * kPer)
+__device__ void level2(const TcArgs& a, int seq, int node, int ntiles, uint2* scratch) {
   const HeadProblem& p = a.p;
   const int lane = threadIdx.x & 31;
   const int k = a.k;
-  const long long ob = ((long long)seq * p.n + node) * k;
-  const uint2* lists = a.cand + ((long long)tile0 * p.n + node) * k;  // list t at lists + t * n * k
-  const long long lstride = (long long)p.n * k;
-  // one round trip: every lane fetches its tiles' (max, sum exp) and list heads
-  float2 st[kL2Tiles / 32];
-  uint32_t head[kL2Tiles / 32];
-  uint32_t mk = 0u;
+  const int kl = k + 1;
+  float bm = -INFINITY, be = 0.f;
+  for (int t = lane; t < ntiles; t += 32) {
+    uint2* src = a.cand + ((long long)(seq * a.tps + t) * p.n + node) * kl;
+    uint2* dst = scratch + t * kl;
+    for (int j0 = 0; !kPollMode && j0 < kl; j0 += 8) {
+      uint2 e[8];
 #pragma unroll
-  for (int c = 0; c < kL2Tiles / 32; ++c) {
-    const int t = lane + 32 * c;
-    st[c] = make_float2(-INFINITY, 0.f);
-    head[c] = 0u;
-    if (t < ntiles) {
-      st[c] = __ldcg(&a.tstat[(long long)(tile0 + t) * p.n + node]);
-      head[c] = __ldcg(&lists[t * lstride]).x;
+      for (int j = 0; j < 8; ++j)
+        if (j0 + j < kl) e[j] = __ldcg(src + j0 + j);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j0 + j < kl) dst[j0 + j] = e[j];
     }
-  }
-  for (int t = lane + kL2Tiles; t < ntiles; t += 32) {  // (more than kL2Tiles tiles: rare)
-    const float x = __ldcg(&a.tstat[(long long)(tile0 + t) * p.n + node]).x;
-    const uint32_t kx = x == -INFINITY ? 0u : float_key(x);
-    mk = kx > mk ? kx : mk;
-  }
+    for (int j0 = 0; kPollMode && j0 < kl; j0 += 8) {
+      uint2 e[8];
+      long long spins = 0;
+      while (true) {
+        bool ok = true;
 #pragma unroll
-  for (int c = 0; c < kL2Tiles / 32; ++c) {
-    const uint32_t kx = st[c].x == -INFINITY ? 0u : float_key(st[c].x);
-    mk = kx > mk ? kx : mk;
-  }
-  const float M = key_value(__reduce_max_sync(0xffffffffu, mk));
-  float es = 0.f;
-#pragma unroll
-  for (int c = 0; c < kL2Tiles / 32; ++c)
-    if (st[c].x != -INFINITY) es += st[c].y * __expf(st[c].x - M);
-  for (int t = lane + kL2Tiles; t < ntiles; t += 32) {
-    const float2 s2 = __ldcg(&a.tstat[(long long)(tile0 + t) * p.n + node]);
-    if (s2.x != -INFINITY) es += s2.y * __expf(s2.x - M);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
-  // threshold: k-th largest list head (k lists each own a value >= T)
-  uint32_t T = 0u;
-  if (ntiles <= 32 && ntiles >= k) T = warp_kth_key(head[0], k);
-  // candidates >= T into the warp scratch; each lane reads its list kChunk
-  // entries at a time (all in flight), stopping once a whole row qualifies nowhere
-  constexpr int kChunk = 8;
-  int cnt = 0;
-  bool overflow = false;
-  for (int t0 = 0; t0 < ntiles; t0 += 32) {
-    const int t = t0 + lane;
-    bool more = true;
-    for (int j0 = 0; j0 < k && more; j0 += kChunk) {
-      uint2 e[kChunk];
-#pragma unroll
-      for (int jj = 0; jj < kChunk; ++jj)
-        e[jj] = (t < ntiles && j0 + jj < k) ? __ldcg(&lists[t * lstride + j0 + jj]) : make_uint2(0u, 0u);
-#pragma unroll
-      for (int jj = 0; jj < kChunk; ++jj) {
-        const bool c = e[jj].x != 0u && e[jj].x >= T;
-        const unsigned bal = __ballot_sync(0xffffffffu, c);
-        if (!bal) { more = false; break; }  // lists are sorted: nothing further qualifies
-        const int slot = cnt + __popc(bal & ((1u << lane) - 1u));
-        if (c && slot < cap) scratch[slot] = e[jj];
-        cnt += __popc(bal);
+        for (int j = 0; j < 8; ++j)
+          if (j0 + j < kl) {
+            e[j] = ld_relaxed_v2(src + j0 + j);
+            ok = ok && e[j].x && e[j].y;
+          }
+        if (ok) break;
+        if (++spins > kSpinLimit) __trap();
       }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j0 + j < kl) {
+          dst[j0 + j] = j0 + j < k ? make_uint2(e[j].x ^ kEncK, e[j].y ^ kEncG) : make_uint2(e[j].x ^ kEncF, e[j].y ^ kEncF);
+          src[j0 + j] = make_uint2(0u, 0u);
+        }
     }
+    const float2 st = make_float2(__uint_as_float(dst[k].x), __uint_as_float(dst[k].y));
+    lse_fold(bm, be, st.x, st.y);
   }
-  overflow = cnt > cap;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, bm, o), e2 = __shfl_xor_sync(0xffffffffu, be, o);
+    lse_fold(bm, be, m2, e2);
+  }
   __syncwarp();
-  uint2 res = make_uint2(0u, 0xffffffffu);
-  if (!overflow) {
-    uint2* best = scratch + cap - kMaxK;  // (cap > kMaxK + candidates: guarded below)
-    if (cnt + kMaxK <= cap) {
-      if (lane < k) best[lane] = make_uint2(0u, 0xffffffffu);
-      __syncwarp();
-      warp_rank_write(scratch, cnt, k, best);
-      __syncwarp();
-      if (lane < k) res = best[lane];
-    } else {
-      overflow = true;
-    }
+  if (threadIdx.x == 0) trace_mark(p.trace, 12);  // warp 0: lists staged
+  int hp[kPer];
+  uint32_t hk[kPer], hg[kPer];
+#pragma unroll
+  for (int c = 0; c < kPer; ++c) {
+    const int t = lane + 32 * c;
+    hp[c] = 0;
+    hk[c] = t < ntiles ? scratch[t * kl].x : 0u;
+    hg[c] = t < ntiles ? scratch[t * kl].y : 0xffffffffu;
   }
-  if (overflow) {
-    // many candidates (e.g. the dense [0, V) comparator): k rounds of a warp
-    // arg-max over the list heads (heads kept in the scratch as positions)
-    int* hpos = reinterpret_cast<int*>(scratch);
-    for (int t = lane; t < ntiles; t += 32) hpos[t] = 0;
-    __syncwarp();
-    for (int r = 0; r < k; ++r) {
-      uint32_t bk = 0u;
-      int32_t bg = 0x7fffffff;
-      int bt = -1;
-      for (int t = lane; t < ntiles; t += 32) {
-        if (hpos[t] >= k) continue;
-        const uint2 e = __ldcg(&lists[t * lstride + hpos[t]]);
-        if (e.x != 0u && key_before(e.x, (int32_t)e.y, bk, bg)) { bk = e.x; bg = (int32_t)e.y; bt = t; }
+  uint2 mine = make_uint2(0u, 0xffffffffu);
+  for (int r = 0; r < k; ++r) {
+    // this lane's best head
+    uint32_t lk = 0u, lg = 0xffffffffu;
+#pragma unroll
+    for (int c = 0; c < kPer; ++c)
+      if (key_before(hk[c], hg[c], lk, lg)) { lk = hk[c]; lg = hg[c]; }
+    const uint32_t wk = __reduce_max_sync(0xffffffffu, lk);
+    if (wk == 0u) break;
+    const uint32_t wg = __reduce_min_sync(0xffffffffu, lk == wk ? lg : 0xffffffffu);
+    if (lane == r) mine = make_uint2(wk, wg);
+#pragma unroll
+    for (int c = 0; c < kPer; ++c)
+      if (hk[c] == wk && hg[c] == wg) {
+        const int t = lane + 32 * c;
+        ++hp[c];
+        const uint2 nx = hp[c] < k ? scratch[t * kl + hp[c]] : make_uint2(0u, 0xffffffffu);
+        hk[c] = nx.x; hg[c] = nx.y;
       }
-      const uint32_t wk = __reduce_max_sync(0xffffffffu, bk);
-      if (wk == 0u) break;
-      const int32_t wg = (int32_t)__reduce_min_sync(0xffffffffu, bk == wk ? (uint32_t)bg : 0x7fffffffu);
-      if (bk == wk && bg == wg && bt >= 0) hpos[bt] += 1;
-      __syncwarp();
-      if (lane == r) res = make_uint2(wk, (uint32_t)wg);
-    }
   }
+  const long long ob = ((long long)seq * p.n + node) * k;
   if (lane < k) {
-    a.topk_logit[ob + lane] = res.x ? key_value(res.x) : -INFINITY;
-    a.topk_id[ob + lane] = res.x ? (int32_t)res.y : -1;
+    a.topk_logit[ob + lane] = mine.x ? key_value(mine.x) : -INFINITY;
+    a.topk_id[ob + lane] = mine.x ? (int32_t)mine.y : -1;
   }
-  if (a.lse && lane == 0) a.lse[(long long)seq * p.n + node] = M == -INFINITY ? -INFINITY : M + logf(es);
+  if (a.lse && lane == 0) a.lse[(long long)seq * p.n + node] = bm == -INFINITY ? -INFINITY : bm + logf(be);
 }
 
-template <int NT>
+// Poll-mode tail of the CTA that owns unit (tile, split): level 1 for nodes
+// split, split + S, ... (one warp each); the tile-0 CTAs then run level 2 for
+// the same nodes.
+__device__ void poll_tail(const TcArgs& a, int tile, int split, const int32_t* ids_s, int m, uint2* smem,
+                          int smem_bytes) {
+  const HeadProblem& p = a.p;
+  const int warp = threadIdx.x >> 5;
+  const int S = a.S;
+  const int seq = tile / a.tps, tin = tile - seq * a.tps;
+  const int row0 = tin * kBM;
+  const int rows = min(kBM, m - row0);
+  const int ntiles = (m + kBM - 1) / kBM;
+  for (int c = split + S * warp; c < p.n; c += S * kWarps) level1<true>(a, tile, c, ids_s, rows, row0, nullptr, nullptr);
+  if (threadIdx.x == 0) trace_mark(p.trace, 10);  // warp 0: level 1 published
+  if (p.trace && (threadIdx.x & 31) == 0)  // last warp of the CTA to publish
+    atomicMax(&p.trace[(long long)blockIdx.x * kTraceSlots + 13], globaltimer());
+  if (tin != 0) return;
+  uint2* scratch = smem + (long long)warp * (smem_bytes / 8 / kWarps);
+  for (int c = split + S * warp; c < p.n; c += S * kWarps) {
+    if (ntiles <= 32) level2<1, true>(a, seq, c, ntiles, scratch);
+    else if (ntiles <= 64) level2<2, true>(a, seq, c, ntiles, scratch);
+    else level2<kMaxL2Lists / 32, true>(a, seq, c, ntiles, scratch);
+  }
+  if (threadIdx.x == 0) trace_mark(p.trace, 11);  // warp 0: level 2 written
+}
+
+// Level 2 (cluster mode, lists complete) for ntiles <= 32: lane t fetches list
+// t's head and lse partial in one round trip; T = k-th largest head (k lists
+// each own an entry >= T); every list's entries >= T (its sorted prefix) are
+// compacted into the warp scratch and ranked by counting.
+__device__ void level2_thr(const TcArgs& a, int seq, int node, int ntiles, uint2* scratch) {
+  const HeadProblem& p = a.p;
+  const int lane = threadIdx.x & 31;
+  const int k = a.k, kl = k + 1;
+  const uint2* lst = a.cand + ((long long)(seq * a.tps + lane) * p.n + node) * kl;
+  uint2 head = make_uint2(0u, 0xffffffffu), st = make_uint2(__float_as_uint(-INFINITY), 0u);
+  if (lane < ntiles) { head = __ldcg(lst); st = __ldcg(lst + k); }
+  float bm = __uint_as_float(st.x), be = __uint_as_float(st.y);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, bm, o), e2 = __shfl_xor_sync(0xffffffffu, be, o);
+    lse_fold(bm, be, m2, e2);
+  }
+  const uint32_t T = ntiles >= k ? warp_kth_key(head.x, k) : 0u;
+  int cnt = 0;
+  for (int j0 = 0; j0 < k; j0 += 8) {
+    uint2 e[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      e[j] = (lane < ntiles && j0 + j < k) ? (j0 + j == 0 ? head : __ldcg(lst + j0 + j)) : make_uint2(0u, 0u);
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const bool c = e[j].x != 0u && e[j].x >= T;
+      const unsigned bal = __ballot_sync(0xffffffffu, c);
+      if (c) scratch[cnt + __popc(bal & ((1u << lane) - 1u))] = e[j];
+      cnt += __popc(bal);
+      any = any || bal;
+    }
+    if (!__any_sync(0xffffffffu, any)) break;  // lists are sorted: nothing further qualifies
+    if (cnt + 32 * 8 > 1024) break;            // (cannot happen: <= k lists reach past T's rank)
+  }
+  uint2* best = scratch + 1024;
+  if (lane < k) best[lane] = make_uint2(0u, 0xffffffffu);
+  __syncwarp();
+  warp_rank_write(scratch, cnt, k, best);
+  __syncwarp();
+  const long long ob = ((long long)seq * p.n + node) * k;
+  if (lane < k) {
+    const uint2 r = best[lane];
+    a.topk_logit[ob + lane] = r.x ? key_value(r.x) : -INFINITY;
+    a.topk_id[ob + lane] = r.x ? (int32_t)r.y : -1;
+  }
+  if (a.lse && lane == 0) a.lse[(long long)seq * p.n + node] = bm == -INFINITY ? -INFINITY : bm + logf(be);
+}
+
+// Cluster-mode tail of the CTA (tile, split): after a cluster barrier, level 1
+// for nodes split, split + S, ... (one warp each, partials over DSMEM); the
+// warp whose list completes a node (per-node arrival counter, release/acquire)
+// runs level 2 for it -- the last arriver finishes the node, nobody waits.
+__device__ void cluster_tail(const TcArgs& a, int tile, int split, const int32_t* ids_s, int m, const float* Pm,
+                             uint2* smem, int smem_bytes) {
+  const HeadProblem& p = a.p;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = a.S;
+  const int seq = tile / a.tps, tin = tile - seq * a.tps;
+  const int row0 = tin * kBM;
+  const int rows = min(kBM, m - row0);
+  const int ntiles = (m + kBM - 1) / kBM;
+  cluster_sync();  // every CTA of the cluster has its partial tile in shared memory
+  if (threadIdx.x == 0) trace_mark(p.trace, 5);
+  // level-2 scratch: the part of the stage area above the partial tile
+  const int pbytes = (p.n * kBM * 4 + 1023) / 1024 * 1024;
+  uint2* scratch = smem + pbytes / 8 + (long long)warp * ((smem_bytes - pbytes) / 8 / kWarps);
+  for (int c = split + S * warp; c < p.n; c += S * kWarps) {
+    level1<false>(a, tile, c, ids_s, rows, row0, Pm, scratch);
+    __syncwarp();
+    unsigned last = 0;
+    if (lane == 0) {
+      last = atom_add_acq_rel(&a.node_ctr[seq * p.n + c], 1u) == (unsigned)(ntiles - 1);
+      if (last) a.node_ctr[seq * p.n + c] = 0u;  // every tile has arrived: reset for the next launch
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {  // the launcher picks cluster mode only for <= 32 tiles per sequence
+      if ((smem_bytes - pbytes) / 8 / kWarps >= 1024 + kMaxK) level2_thr(a, seq, c, ntiles, scratch);
+      else level2<1, false>(a, seq, c, ntiles, scratch);
+    }
+  }
+  if (threadIdx.x == 0) trace_mark(p.trace, 10);
+  cluster_sync();  // peers are done reading this CTA's partial tile
+}
+
+template <int NT, int MODE>  // one instantiation per mode: only its own tail is compiled in
 __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
   using C = Cfg<NT>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -392,7 +763,7 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
   // bars[0..S) full, [S..2S) empty, [2S] tmem_full, [2S+1] tmem_empty
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::kStages + 2);
   __shared__ int32_t ids_s[kBM];   // the unit's row ids
-  __shared__ int sh_last[kWarps];
+  __shared__ int sh_m;
 
   const HeadProblem& p = a.p;
   const int tid = threadIdx.x;
@@ -401,6 +772,7 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
   const int S = a.S;
 
   if (tid == 0) trace_mark(p.trace, 0);  // start
+  if (tid == 0 && p.trace) p.trace[(long long)blockIdx.x * kTraceSlots + 14] = clock64();
   if (tid == 0) {
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(smem_u32(&bars[s]), kLoaders);          // full: every loader thread arrives
@@ -431,30 +803,30 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
   // lr + 64 (lr = t >> 3) of every W stage, and of H rows lr + 64 i < NT.
   const int lr = tid >> 3;
   const uint32_t swz = (uint32_t)(((tid & 7) ^ (lr & 7)) << 4);
-  uint2* wscratch = reinterpret_cast<uint2*>(smem + C::kPBytes + warp * C::kWarpScratch);
-  const int wcap = C::kWarpScratch / 8;
-  const float* Pm = reinterpret_cast<const float*>(smem);  // partial tile [NT][128] after the MMAs
 
   const int tiles_g = p.batch * a.tps;
-  const int split = S > 1 ? (int)cluster_ctarank() : 0;
+  const int split = S > 1 ? (int)blockIdx.x % S : 0;
   const int first = S > 1 ? (int)blockIdx.x / S : (int)blockIdx.x;
   const int step = S > 1 ? tiles_g : (int)gridDim.x;
   int it = 0;      // pipeline iteration counter across units
   int local = 0;   // units processed by this CTA
   for (int tile = first; tile < tiles_g; tile += step) {
     const int seq = tile / a.tps, tin = tile - (tile / a.tps) * a.tps;
-    const int m = clamp_nact(p, seq);
     const int row0 = tin * kBM;
+    // one round trip: the tile's ids (rows past n_active are never dereferenced)
+    // and n_active
+    if (tid < kBM) ids_s[tid] = row0 + tid < p.max_ids ? __ldcg(p.ids_base + (long long)seq * p.ids_stride + row0 + tid) : 0;
+    if (tid == kBM) sh_m = clamp_nact(p, seq);
+    __syncthreads();
+    if (tid == 0 && local == 0) trace_mark(p.trace, 7);  // ids + n_active in shared memory
+    const int m = sh_m;
     const int rows = min(kBM, m - row0);
-    if (rows <= 0) continue;  // the whole cluster (same tile) skips together
-    const int ntiles = (m + kBM - 1) / kBM;
+    if (rows <= 0) {  // past n_active: every CTA of the tile skips it
+      __syncthreads();
+      continue;
+    }
     const int kb0 = split * KB / S, kb1 = (split + 1) * KB / S;
     const int nk = kb1 - kb0;
-    if (tid < kBM) {
-      const int32_t* idp = p.ids_base + (long long)seq * p.ids_stride + row0;
-      ids_s[tid] = __ldg(idp + min(tid, rows - 1));
-    }
-    __syncthreads();
 
     if (warp < kLoadWarps) {
       // ---------------- producers: gather rows of W_head + H into SW128 stages
@@ -495,14 +867,16 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
         }
       }
       if (tid == 0 && local == 0) trace_mark(p.trace, 3);  // all loads issued and landed
-      // ---------------- epilogue: TMEM -> registers -> partial tile P in shared memory
+      // ---------------- epilogue: TMEM -> registers -> this unit's slot of P
       mbar_wait(smem_u32(&bars[2 * C::kStages]), local & 1);
       tc_fence_after();
       if (tid == 0 && local == 0) trace_mark(p.trace, 4);  // last MMA done
       const int lg = warp & 3, cgp = warp >> 2;   // TMEM lane group, column group
       const int r = lg * 32 + lane;               // TMEM lane == tile row
       const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16);
-      float* Pw = reinterpret_cast<float*>(smem) + r;
+      // per column, the 32 lanes of a warp store 128 consecutive bytes
+      float* Pw = MODE == kModeCluster ? reinterpret_cast<float*>(smem) + r
+                                         : a.part + (((long long)tile * S + split) * p.n) * kBM + r;
       if (cgp < C::kColGroups) {
 #pragma unroll 1
         for (int c0 = cgp * 16; c0 < NT && c0 < p.n; c0 += 16 * C::kColGroups) {
@@ -510,7 +884,12 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
           tmem_ld16(taddr + c0, v);
 #pragma unroll
           for (int c = 0; c < 16; ++c)
-            if (c0 + c < p.n) Pw[(c0 + c) * kBM] = v[c];
+            if (c0 + c < p.n) {
+              if (MODE == kModePoll)  // strong store: visible to the polling CTAs without a fence
+                st_relaxed_f32(Pw + (c0 + c) * kBM, __uint_as_float(__float_as_uint(v[c] == 0.f ? 0.f : v[c]) ^ kEncF));
+              else
+                Pw[(c0 + c) * kBM] = v[c];
+            }
         }
       }
       tc_fence_before();
@@ -537,79 +916,80 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
         }
         __syncwarp();
       }
-      // the MMA warp joins below once the epilogue has drained TMEM
+      // the MMA warp waits until the epilogue has drained TMEM
       mbar_wait(smem_u32(&bars[2 * C::kStages + 1]), local & 1);
     }
     it += nk;
-
-    // ---------------- split-K reduction over the cluster, level-1 top-k
-    __syncthreads();  // P complete in this CTA
-    if (S > 1) cluster_sync();  // ... and in every CTA of the cluster
-    if (tid == 0 && local == 0) trace_mark(p.trace, 5);  // partials complete
-    if (lane == 0) sh_last[warp] = 0;
-    for (int c = split + S * warp; c < p.n; c += S * kWarps) {
-      // node c, rows 4*lane .. 4*lane+3: sum of the S partials in split order
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      const uint32_t la = smem_u32(Pm + c * kBM + 4 * lane);
-      if (S == 1) {
-        acc = *reinterpret_cast<const float4*>(Pm + c * kBM + 4 * lane);
-      } else {
-        float4 x[kMaxCluster];
-#pragma unroll
-        for (int s2 = 0; s2 < kMaxCluster; ++s2)
-          if (s2 < S) x[s2] = ld_dsmem_v4(mapa_shared(la, (uint32_t)s2));
-#pragma unroll
-        for (int s2 = 0; s2 < kMaxCluster; ++s2)
-          if (s2 < S) { acc.x += x[s2].x; acc.y += x[s2].y; acc.z += x[s2].z; acc.w += x[s2].w; }
-      }
-      const float v[4] = {acc.x, acc.y, acc.z, acc.w};
-      const int32_t g[4] = {ids_s[4 * lane], ids_s[4 * lane + 1], ids_s[4 * lane + 2], ids_s[4 * lane + 3]};
-      if (p.logits) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (4 * lane + i < rows) p.logits[((long long)seq * p.n + c) * p.max_ids + row0 + 4 * lane + i] = v[i];
-      }
-      uint2* cout = a.cand + ((long long)tile * p.n + c) * a.k;
-      level1(v, g, 4 * lane, rows, a.k, wscratch, cout, &a.tstat[(long long)tile * p.n + c]);
-      // level 2: the warp whose list completes the node merges it.  The warp's
-      // list is published by lane 0's release (after the warp barrier); the
-      // last arriver's acquire makes every tile's list visible.
-      __syncwarp();
-      unsigned last = 0;
-      if (lane == 0) {
-        last = atom_add_acq_rel(&a.node_ctr[seq * p.n + c], 1u) == (unsigned)(ntiles - 1);
-        if (last) a.node_ctr[seq * p.n + c] = 0u;  // every other tile has arrived: reset for the next launch
-      }
-      last = __shfl_sync(0xffffffffu, last, 0);
-      if (last) level2(a, seq, c, seq * a.tps, ntiles, wscratch, wcap);
-    }
-    if (tid == 0 && local == 0) trace_mark(p.trace, 6);  // level 1 (+ merges) done
-    if (S > 1) cluster_sync();  // peers are done reading this CTA's partials
-    __syncthreads();            // P / scratch free for the next unit
+    __syncthreads();  // ids_s free for the next unit
     ++local;
   }
 
-  if (tid == 0) trace_mark(p.trace, 8);  // done
   tc_fence_before();
-  __syncthreads();
+  __syncthreads();  // every partial of this CTA is stored; TMEM drained
   if (warp == kLoadWarps) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::kTmemCols));
   }
+  if (tid == 0) trace_mark(p.trace, 9);  // drained
+  if (MODE == kModeCluster) {
+    if (local > 0)
+      cluster_tail(a, first, split, ids_s, sh_m, reinterpret_cast<const float*>(smem), reinterpret_cast<uint2*>(smem),
+                   C::kStageArea);
+    if (tid == 0) trace_mark(p.trace, 8);  // done
+    return;
+  }
+  if (MODE == kModePoll) {
+    if (local > 0) poll_tail(a, first, split, ids_s, sh_m, reinterpret_cast<uint2*>(smem), C::kStageArea);
+    if (tid == 0) trace_mark(p.trace, 8);  // done
+    if (tid == 0 && p.trace) p.trace[(long long)blockIdx.x * kTraceSlots + 15] = clock64();
+    return;
+  }
+  // ---------------- grid arrival; finishers wait for the generation to change
+  const int npairs = p.batch * p.n;
+  const bool finisher = (int)blockIdx.x < npairs;
+  __shared__ unsigned sh_gen;
+  if (tid == 0) {
+    const unsigned old = atom_add_acq_rel(a.grid_word, 1u);
+    const unsigned cmask = (1u << kCountBits) - 1u;
+    if ((old & cmask) == gridDim.x - 1u) red_add_release(a.grid_word, (1u << kCountBits) - gridDim.x);
+    else if (finisher)
+      while ((ld_acquire(a.grid_word) >> kCountBits) == (old >> kCountBits)) {}
+  }
+  if (!finisher) {
+    if (tid == 0) trace_mark(p.trace, 8);  // done
+    return;
+  }
+  __syncthreads();
+  if (tid == 0) trace_mark(p.trace, 5);  // all partials visible
+  // stage area: [0, kSpBytes) partial slices of a round, then the per-warp lists
+  constexpr int kListBytes = kWarps * kMaxK * 8 + kWarps * 8;
+  constexpr int kSpBytes = (C::kStageArea - kListBytes) / 1024 * 1024;
+  int rr = kSpBytes / (4 * S) / kBM * kBM;
+  if (rr > kThreads * kFinRows / kBM * kBM) rr = kThreads * kFinRows / kBM * kBM;
+  float* sp = reinterpret_cast<float*>(smem);
+  uint2* wl = reinterpret_cast<uint2*>(smem + kSpBytes);                         // [kWarps][k]
+  float2* wm = reinterpret_cast<float2*>(smem + kSpBytes + kWarps * kMaxK * 8);  // [kWarps]
+  for (int pr = blockIdx.x; pr < npairs; pr += gridDim.x) finish_node(a, pr / p.n, pr % p.n, sp, rr, wl, wm);
+  if (tid == 0) trace_mark(p.trace, 8);  // done
+  (void)sh_gen;
 }
 
 struct ScratchLayout {
-  size_t node_ctr, cand, tstat, total;
+  size_t grid_word, node_ctr, part, cand, total;
 };
 
+// S * tiles_g <= kMaxSMs whenever S > 1, and S = 1 otherwise: the partial
+// buffer holds max(kMaxSMs, tiles) tiles of n x 128 floats.
 inline ScratchLayout scratch_layout(int batch, int max_ids, int n) {
   const size_t tiles = (size_t)batch * ((max_ids + kBM - 1) / kBM);
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
   ScratchLayout L;
   size_t off = 0;
-  L.node_ctr = off; off += al(sizeof(unsigned) * (size_t)batch * n);
-  L.cand = off;     off += al(tiles * (size_t)n * kMaxK * sizeof(uint2));
-  L.tstat = off;    off += al(tiles * (size_t)n * sizeof(float2));
+  L.grid_word = off; off += al(sizeof(unsigned));
+  L.node_ctr = off;  off += al(sizeof(unsigned) * (size_t)batch * n);
+  L.part = off;      off += al((tiles > (size_t)kMaxSMs ? tiles : (size_t)kMaxSMs) * n * kBM * sizeof(float));
+  const size_t ctiles = tiles < (size_t)kMaxSMs ? tiles : (size_t)kMaxSMs;  // poll mode: tiles_g <= #SMs
+  L.cand = off;      off += al(ctiles * n * (kMaxK + 1) * sizeof(uint2));
   L.total = off;
   return L;
 }
@@ -621,7 +1001,12 @@ cudaError_t launch_nt(const HeadProblem& p, int k, float* topk_logit, int32_t* t
   static bool attr = false;
   if (!attr) {
     cudaError_t e =
-        cudaFuncSetAttribute(head_tc_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+        cudaFuncSetAttribute(head_tc_kernel<NT, kModeFinish>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(head_tc_kernel<NT, kModePoll>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(head_tc_kernel<NT, kModeCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               C::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -630,9 +1015,10 @@ cudaError_t launch_nt(const HeadProblem& p, int k, float* topk_logit, int32_t* t
   char* sc = (char*)scratch;
   TcArgs a;
   a.p = p;
-  a.node_ctr = (unsigned*)(sc + L.node_ctr);
+  a.grid_word = (unsigned*)(sc + L.grid_word);
+  a.part = (float*)(sc + L.part);
   a.cand = (uint2*)(sc + L.cand);
-  a.tstat = (float2*)(sc + L.tstat);
+  a.node_ctr = (unsigned*)(sc + L.node_ctr);
   a.topk_logit = topk_logit;
   a.topk_id = topk_id;
   a.lse = lse;
@@ -641,12 +1027,19 @@ cudaError_t launch_nt(const HeadProblem& p, int k, float* topk_logit, int32_t* t
   const int G = num_sms < kMaxSMs ? num_sms : kMaxSMs;
   const int tiles_g = p.batch * a.tps;
   const int KB = p.d / kBK;
-  // Largest cluster (K-split) size S <= 8 whose tiles_g clusters are all
-  // co-resident in one wave (GPC packing decides, so ask the runtime; cached).
+  // Mode.  One unit per CTA (tiles_g <= #SMs): prefer clusters of S K-splits
+  // per tile (the largest S <= 8 whose tiles_g clusters are all co-resident,
+  // so the DSMEM reduction never waits for a second wave); else S = #SMs /
+  // tiles_g with the L2 hand-off (poll mode); else persistent finishers.
   static int max_clusters[kMaxCluster + 1] = {0};
-  int S = 1;
-  if (tiles_g < G) {
-    for (int s = kMaxCluster; s >= 2; --s) {
+  static int env_mode = -2;
+  if (env_mode == -2) {
+    const char* e = getenv("NANOSPEC_HEAD_MODE");  // debug: force finish / poll / cluster
+    env_mode = e ? atoi(e) : -1;
+  }
+  int S = 1, mode = kModeFinish;
+  if (tiles_g <= G && a.tps <= kMaxL2Lists && (long long)a.tps * (k + 1) * 8 <= (C::kStageArea - p.n * kBM * 4 - 1024) / kWarps) {
+    for (int s = kMaxCluster; s >= 2 && a.tps <= 32 && env_mode != kModePoll && env_mode != kModeFinish; --s) {
       if (s > KB || s * tiles_g > G) continue;
       if (max_clusters[s] == 0) {
         cudaLaunchConfig_t q = {};
@@ -661,19 +1054,26 @@ cudaError_t launch_nt(const HeadProblem& p, int k, float* topk_logit, int32_t* t
         q.attrs = &ca;
         q.numAttrs = 1;
         int nc = 0;
-        if (cudaOccupancyMaxActiveClusters(&nc, head_tc_kernel<NT>, &q) != cudaSuccess || nc <= 0) {
+        if (cudaOccupancyMaxActiveClusters(&nc, head_tc_kernel<NT, kModeCluster>, &q) != cudaSuccess || nc <= 0) {
           (void)cudaGetLastError();
           nc = -1;
         }
         max_clusters[s] = nc;
       }
-      if (max_clusters[s] >= tiles_g) { S = s; break; }
+      if (max_clusters[s] >= tiles_g) { S = s; mode = kModeCluster; break; }
+    }
+    if (mode != kModeCluster && env_mode != kModeFinish) {
+      S = G / tiles_g;
+      if (S > KB) S = KB;
+      if (S > kMaxSplit) S = kMaxSplit;
+      mode = kModePoll;
     }
   }
   a.S = S;
+  a.mode = mode;
 
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(S > 1 ? tiles_g * S : (tiles_g < G ? tiles_g : G));
+  cfg.gridDim = dim3(mode != kModeFinish ? tiles_g * S : (tiles_g < G ? tiles_g : G));
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = C::kSmemBytes;
   cfg.stream = stream;
@@ -682,7 +1082,7 @@ cudaError_t launch_nt(const HeadProblem& p, int k, float* topk_logit, int32_t* t
   attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attrs[na].val.programmaticStreamSerializationAllowed = 1;
   ++na;
-  if (S > 1) {
+  if (mode == kModeCluster) {
     attrs[na].id = cudaLaunchAttributeClusterDimension;
     attrs[na].val.clusterDim.x = S;
     attrs[na].val.clusterDim.y = 1;
@@ -691,12 +1091,15 @@ cudaError_t launch_nt(const HeadProblem& p, int k, float* topk_logit, int32_t* t
   }
   cfg.attrs = attrs;
   cfg.numAttrs = na;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, head_tc_kernel<NT>, a);
+  auto kern = mode == kModeCluster ? head_tc_kernel<NT, kModeCluster>
+              : mode == kModePoll  ? head_tc_kernel<NT, kModePoll>
+                                   : head_tc_kernel<NT, kModeFinish>;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
   if (e != cudaSuccess) {
     (void)cudaGetLastError();
     cfg.attrs = attrs + 1;  // without PDL
     cfg.numAttrs = na - 1;
-    e = cudaLaunchKernelEx(&cfg, head_tc_kernel<NT>, a);
+    e = cudaLaunchKernelEx(&cfg, kern, a);
   }
   return e;
 }

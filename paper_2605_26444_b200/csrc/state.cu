@@ -221,17 +221,18 @@ __global__ void __launch_bounds__(512) state_append_kernel(AppendArgs args) {
 }
 
 // Per-step fast path of a2 (rule R1, no reset, both lists together <= 512 ids
-// and <= W_max): one CTA per sequence, O(changes) work.
-//  * tuple(.) dedup: shared-memory hash of (list, id) -> first position;
-//  * the evicted ring slots are read, and the net window-count change of every
-//    touched id (appends - evictions) is formed in a shared-memory hash, so one
-//    returning atomicAdd per distinct id tells which ids leave I (count -> 0)
-//    and which enter it (0 -> count);
-//  * slot table (pos[g] = slot of g): entering ids take the slots of leaving
-//    ids, extra entries are appended, surplus holes are refilled from the tail,
-//    so ids[0, n_active) stays dense and every other id keeps its slot.
-// Global round trips: {meta, lists} -> ring slots -> count atomics -> slots of
-// the leaving ids (-> ids of the tail movers when I shrinks).
+// and <= W_max): one CTA per sequence, O(changes) work, three dependent global
+// round trips (the single writer of a sequence needs no global atomics):
+//   RT1  meta (total, n_active) + the two lists;
+//        tuple(.) dedup in a shared-memory hash, block scan -> ring slots;
+//   RT2  evicted ring slots, cnt[] of the appended ids, the last L ids[] slots
+//        (candidates to move when I shrinks);
+//   RT3  cnt[] and pos[] of the evicted ids;
+// then every touched id's window count is updated by its net change
+// (appends - evictions): count 0 -> >0 enters I, >0 -> 0 leaves it.  Slot
+// table (pos[g] = slot of g in ids[]): entering ids take the slots of leaving
+// ids, extra entries are appended, surplus holes are refilled from the tail,
+// so ids[0, n_active) stays dense and every other id keeps its slot.
 constexpr int kFastThreads = 512;
 constexpr int kHashSlots = 2048;
 
@@ -250,11 +251,14 @@ __device__ __forceinline__ int hash_insert(int32_t* keys, int32_t key) {
 }
 
 __global__ void __launch_bounds__(kFastThreads) state_update_fast_kernel(AppendArgs args, unsigned long long* trace) {
-  __shared__ int32_t hkey[kHashSlots];   // dedup table, then net-delta table
-  __shared__ int32_t hval[kHashSlots];
+  __shared__ int32_t hkey[kHashSlots];   // dedup table, then the touched-id table
+  __shared__ int32_t hval[kHashSlots];   // first position, then net count change
+  __shared__ int32_t hcnt[kHashSlots];   // window count before this update
+  __shared__ int32_t hpos[kHashSlots];   // slot before this update (evicted ids)
   __shared__ int32_t leave[kFastThreads];  // local ids leaving I
   __shared__ int32_t enter[kFastThreads];  // local ids entering I
   __shared__ int32_t hole[kFastThreads];   // their former slots
+  __shared__ int32_t tail[kFastThreads];   // tail[j] = ids[n_old - 1 - j]
   __shared__ int32_t mover_slot[kFastThreads];
   __shared__ int32_t low_hole[kFastThreads];
   __shared__ unsigned char tail_hole[kFastThreads];
@@ -279,6 +283,7 @@ __global__ void __launch_bounds__(kFastThreads) state_update_fast_kernel(AppendA
   int32_t* cnt = sv.cnt + (long long)seq * sv.v_local;
   int32_t* pos = sv.pos + (long long)seq * sv.v_local;
   int32_t* ids = sv.ids + (long long)seq * W;
+  // ---- RT1: meta + lists
   if (tid == 0) {
     sh_total = sv.meta[seq].total;
     sh_nact = sv.meta[seq].n_active;
@@ -303,26 +308,50 @@ __global__ void __launch_bounds__(kFastThreads) state_update_fast_kernel(AppendA
   int nk;
   const int sp = block_exclusive_scan(keep ? 1 : 0, sh_scan, &nk);
   const long long total = sh_total;
+  const int n_old = sh_nact;
+  // ---- RT2: evicted slots, counts of the appended ids, tail of the slot table
   int slot = (int)(total % W) + sp;  // sp < W: one wrap at most
   if (slot >= W) slot -= W;
-  int32_t old = -1;
+  const bool e_loc = keep && is_local(sv, e);
+  const int32_t le = e_loc ? local_of(sv, e) : -1;
+  int32_t old = -1, ce = 0, tl = -1;
   if (keep && total + sp >= W) old = ring[slot];
+  if (e_loc) ce = cnt[le];
+  if (tid < L && n_old - 1 - tid >= 0) tl = ids[n_old - 1 - tid];
+  const bool o_loc = old >= 0 && is_local(sv, old);
+  const int32_t lo = o_loc ? local_of(sv, old) : -1;
+  // ---- RT3 (issued right away; independent of the shared-memory work below)
+  int32_t co = 0, po = 0;
+  if (o_loc) { co = cnt[lo]; po = pos[lo]; }
   if (keep) ring[slot] = e;
+  if (tid < L) tail[tid] = tl;
   for (int h = tid; h < kHashSlots; h += kFastThreads) { hkey[h] = -1; hval[h] = 0; }
   __syncthreads();
   if (tid == 0) trace_mark(trace, 11);  // state: ring slots read
-  // ---- net window-count change per touched local id
-  if (old >= 0 && is_local(sv, old)) atomicSub(&hval[hash_insert(hkey, local_of(sv, old))], 1);
-  if (keep && is_local(sv, e)) atomicAdd(&hval[hash_insert(hkey, local_of(sv, e))], 1);
+  // ---- net window-count change per touched local id, with its prior count / slot
+  if (e_loc) {
+    const int h = hash_insert(hkey, le);
+    atomicAdd(&hval[h], 1);
+    hcnt[h] = ce;
+  }
+  if (o_loc) {
+    const int h = hash_insert(hkey, lo);
+    atomicSub(&hval[h], 1);
+    hcnt[h] = co;  // every writer of a slot stores the same pre-update value
+    hpos[h] = po;
+  }
   __syncthreads();
   for (int h = tid; h < kHashSlots; h += kFastThreads) {
     const int32_t l = hkey[h], dlt = hval[h];
     if (l < 0 || dlt == 0) continue;
-    const int32_t before = atomicAdd(&cnt[l], dlt);
+    const int32_t before = hcnt[h];
     const int32_t after = before + dlt;
+    cnt[l] = after;
     if (before > 0 && after == 0) {
       atomicAnd(&bm[l >> 5], ~(1u << (l & 31)));
-      leave[atomicAdd(&sh_nl, 1)] = l;
+      const int q = atomicAdd(&sh_nl, 1);
+      leave[q] = l;
+      hole[q] = hpos[h];  // a leaving id was evicted, so its slot was read in RT3
     } else if (before == 0 && after > 0) {
       atomicOr(&bm[l >> 5], 1u << (l & 31));
       enter[atomicAdd(&sh_ne, 1)] = l;
@@ -332,15 +361,19 @@ __global__ void __launch_bounds__(kFastThreads) state_update_fast_kernel(AppendA
   if (tid == 0) trace_mark(trace, 12);  // state: counts updated
   // ---- slot table
   const int nl = sh_nl, ne = sh_ne;
-  const int n_old = sh_nact, n_new = n_old - nl + ne;
-  if (tid < nl) hole[tid] = pos[leave[tid]];
+  const int n_new = n_old - nl + ne;
   if (tid < n_old - n_new) tail_hole[tid] = 0;
   __syncthreads();
   const int32_t gmul = sv.n_shards <= 1 ? 1 : sv.n_shards, gadd = sv.n_shards <= 1 ? 0 : sv.rank;
   if (tid < ne) {  // entering ids: a freed slot, or a new slot at the end
     const int s2 = tid < nl ? hole[tid] : n_old + (tid - nl);
-    ids[s2] = enter[tid] * gmul + gadd;
+    const int32_t g = enter[tid] * gmul + gadd;
+    ids[s2] = g;
     pos[enter[tid]] = s2;
+    // a hole in the tail [n_new, n_old) refilled here is then moved down as a
+    // live entry: keep the prefetched tail current
+    const int j = n_old - 1 - s2;
+    if (j >= 0 && j < L) tail[j] = g;
   }
   if (nl > ne) {
     // I shrinks by d = nl - ne: holes hole[ne..nl) below n_new are refilled
@@ -355,7 +388,7 @@ __global__ void __launch_bounds__(kFastThreads) state_update_fast_kernel(AppendA
     if (tid < d && !tail_hole[tid]) mover_slot[atomicAdd(&sh_nm, 1)] = n_new + tid;
     __syncthreads();
     if (tid < sh_nm) {  // sh_nm == sh_nh; any pairing works
-      const int32_t g = ids[mover_slot[tid]];
+      const int32_t g = tail[n_old - 1 - mover_slot[tid]];  // d <= L: inside the prefetched tail
       const int dst = low_hole[tid];
       ids[dst] = g;
       pos[local_of(sv, g)] = dst;

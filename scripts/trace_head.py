@@ -15,8 +15,8 @@ import paper_2605_26444_b200 as P  # noqa: E402
 from paper_2605_26444_b200 import _native as N  # noqa: E402
 from synthetic import inputs as SI  # noqa: E402
 
-EVENTS = ["start", "dep_ok", "rowptr", "loads_landed", "mma_done", "partials_ready", "level1_done", "-",
-          "done"]
+EVENTS = ["start", "dep_ok", "rowptr", "loads_landed", "mma_done", "fin_go", "-", "ids_ready",
+          "done", "drained", "l1|fin_staged", "l2|fin_summed", "l2staged|fin_warp_topk", "l1_all|fin_lists"]
 
 
 def main():
@@ -63,9 +63,12 @@ def main():
         print(f"=== {mode} (m={args.m}, n={args.n}); event-timed call: "
               f"{np.median([r[0] for r in rows]):.2f} us median of {args.reps}")
         ev_us, t, t0 = rows[-1]
-        print("  candidates per task:", sorted(int(x) for x in t[:, 15] if x > 0)[:12], "...")
-        t[:, 13:16] = 0
-        t[:, 13] = 0
+        cyc = t[:, 15] - t[:, 14]
+        ns = t[:, 8] - t[:, 0]
+        ok = (t[:, 15] > 0) & (ns > 0)
+        if ok.any():
+            print(f"  SM clock during the call: {np.median(cyc[ok] / ns[ok]):.3f} GHz (median over CTAs)")
+        t[:, 14:16] = 0
 
         for e, name in enumerate(EVENTS):
             col = t[:, e]
