@@ -214,9 +214,17 @@ nanospec_status nanospec_merge_topk(const float* d_cand_logit, const int32_t* d_
  * (off, the default).  While set, the fused tensor-core head writes the
  * %globaltimer (ns) of its phases, CTA b at d_buf[b*16 + e]: 0 start,
  * 1 dependency resolved, 2 row pointers ready, 3 last load landed, 4 last MMA
- * done, 5 epilogue done, 6 grid barrier passed, 7 top-k inputs staged,
- * 8 top-k done.  Process-wide; not thread-safe; for profiling only. */
+ * done, 5 reduction inputs visible, 7 ids staged, 8 done, 9 drained,
+ * 10-13 tail phases (scripts/trace_head.py names them), 14/15 clock64 at
+ * start / end.  Process-wide; not thread-safe; for profiling only. */
 nanospec_status nanospec_debug_set_trace(unsigned long long* d_buf, int32_t ctas);
+
+/* Debug: force the fused tensor-core head's split-K reduction mode for the
+ * following calls: -1 automatic (default), 0 persistent CTAs + grid barrier +
+ * one finisher CTA per (sequence, node), 1 one unit per CTA with L2 hand-off
+ * (poll), 2 clusters of K-split CTAs with DSMEM reduction.  A forced mode the
+ * shape cannot use falls back to the automatic choice.  Process-wide; tests. */
+nanospec_status nanospec_debug_set_head_mode(int32_t mode);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -22,6 +22,7 @@ EXPORTS = [
     "nanospec_state_read", "nanospec_state_check", "nanospec_state_ids_ptr", "nanospec_state_n_active_ptr",
     "nanospec_head_scratch_bytes", "nanospec_draft_logits_topk", "nanospec_draft_logits_topk_ex",
     "nanospec_logits_topk_ids", "nanospec_merge_topk", "nanospec_debug_set_trace",
+    "nanospec_debug_set_head_mode",
 ]
 
 
@@ -68,6 +69,7 @@ def lib():
                                            ctypes.c_int, vp]
     L.nanospec_merge_topk.argtypes = [vp, vp, vp, i32, i32, i32, vp, vp, vp, vp]
     L.nanospec_debug_set_trace.argtypes = [vp, i32]
+    L.nanospec_debug_set_head_mode.argtypes = [i32]
     _lib = L
     return L
 

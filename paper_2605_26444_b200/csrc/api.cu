@@ -325,6 +325,12 @@ nanospec_status nanospec_debug_set_trace(unsigned long long* d_buf, int32_t ctas
   return NANOSPEC_OK;
 }
 
+nanospec_status nanospec_debug_set_head_mode(int32_t mode) {
+  if (mode < -1 || mode > 2) return NANOSPEC_EINVAL;
+  set_head_tc_mode(mode);
+  return NANOSPEC_OK;
+}
+
 nanospec_status nanospec_merge_topk(const float* d_cand_logit, const int32_t* d_cand_id, const float* d_cand_lse,
                                     int32_t n_shards, int32_t n_rows, int32_t k, float* d_out_logit,
                                     int32_t* d_out_id, float* d_out_lse, cudaStream_t stream) {

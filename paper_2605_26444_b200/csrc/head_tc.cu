@@ -35,7 +35,6 @@
 // reads TMEM lanes 32*(w%4).. and a quarter of the columns); warp 16 allocates
 // TMEM and one lane issues the MMAs.  All 17 warps run the reduction / top-k.
 #include <math.h>
-#include <stdlib.h>
 
 #include "common.cuh"
 #include "internal.h"
@@ -506,6 +505,40 @@ __device__ void level1(const TcArgs& a, int tile, int node, const int32_t* ids_s
   }
   const int r0 = 4 * lane;
   uint32_t key[4], gid[4];
+  if (!kPollMode) {
+    // lse partial + threshold selection written straight to the tile's list
+    uint32_t lmk = 0u;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const bool ok = r0 + i < rows;
+      key[i] = ok ? float_key(v[i]) : 0u;
+      gid[i] = ok ? (uint32_t)ids_s[r0 + i] : 0xffffffffu;
+      lmk = key[i] > lmk ? key[i] : lmk;
+      if (ok && p.logits) p.logits[((long long)(tile / a.tps) * p.n + node) * p.max_ids + row0 + r0 + i] = v[i];
+    }
+    const float M = key_value(__reduce_max_sync(0xffffffffu, lmk));
+    float es = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (key[i]) es += __expf(v[i] - M);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
+    const uint32_t T = warp_kth_key(lmk, k);
+    int cnt = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const bool c = key[i] != 0u && key[i] >= T;
+      const unsigned bal = __ballot_sync(0xffffffffu, c);
+      if (c) scratch[cnt + __popc(bal & ((1u << lane) - 1u))] = make_uint2(key[i], gid[i]);
+      cnt += __popc(bal);
+    }
+    uint2* out = a.cand + ((long long)tile * p.n + node) * (k + 1);
+    if (lane < k) out[lane] = make_uint2(0u, 0xffffffffu);  // padding when rows < k
+    if (lane == 0) out[k] = make_uint2(__float_as_uint(M), __float_as_uint(es));
+    __syncwarp();
+    warp_rank_write(scratch, cnt, k, out);
+    return;
+  }
   float mloc = -INFINITY;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -974,6 +1007,8 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
   (void)sh_gen;
 }
 
+int g_head_mode = -1;  // -1 auto; kModeFinish / kModePoll / kModeCluster forced where feasible
+
 struct ScratchLayout {
   size_t grid_word, node_ctr, part, cand, total;
 };
@@ -1032,11 +1067,7 @@ cudaError_t launch_nt(const HeadProblem& p, int k, float* topk_logit, int32_t* t
   // so the DSMEM reduction never waits for a second wave); else S = #SMs /
   // tiles_g with the L2 hand-off (poll mode); else persistent finishers.
   static int max_clusters[kMaxCluster + 1] = {0};
-  static int env_mode = -2;
-  if (env_mode == -2) {
-    const char* e = getenv("NANOSPEC_HEAD_MODE");  // debug: force finish / poll / cluster
-    env_mode = e ? atoi(e) : -1;
-  }
+  const int env_mode = g_head_mode;  // debug override (nanospec_debug_set_head_mode), -1 = auto
   int S = 1, mode = kModeFinish;
   if (tiles_g <= G && a.tps <= kMaxL2Lists && (long long)a.tps * (k + 1) * 8 <= (C::kStageArea - p.n * kBM * 4 - 1024) / kWarps) {
     for (int s = kMaxCluster; s >= 2 && a.tps <= 32 && env_mode != kModePoll && env_mode != kModeFinish; --s) {
@@ -1107,6 +1138,8 @@ cudaError_t launch_nt(const HeadProblem& p, int k, float* topk_logit, int32_t* t
 }  // namespace
 
 size_t head_tc_scratch_bytes(int batch, int max_ids, int n) { return scratch_layout(batch, max_ids, n).total; }
+
+void set_head_tc_mode(int mode) { g_head_mode = mode; }
 
 cudaError_t launch_head_tc(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse,
                            void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t stream) {

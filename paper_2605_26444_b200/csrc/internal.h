@@ -42,6 +42,8 @@ cudaError_t launch_head_simt(const HeadProblem& p, int num_sms, cudaStream_t str
 cudaError_t launch_head_tc(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse,
                            void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t stream);
 size_t head_tc_scratch_bytes(int batch, int max_ids, int n);
+// Debug: force the fused head's reduction mode (-1 auto, 0 finisher, 1 poll, 2 cluster).
+void set_head_tc_mode(int mode);
 
 // Phase 2 (a5): per (sequence, node) top-k by (value desc, id asc) + lse.
 cudaError_t launch_select_topk(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse,

@@ -182,3 +182,55 @@ def test_batch_of_sequences(cuda_ok, llama, impl):
         v_ref, id_ref = O.topk(z_ref, ids, k)
         check_topk(v[b].cpu().numpy(), i[b].cpu().numpy(), z_ref, A, ids, v_ref, id_ref, f"seq {b}")
         check_lse(l[b].cpu().numpy(), O.lse(z_ref), f"seq {b}")
+
+
+@pytest.fixture
+def head_mode():
+    """Force the fused head's reduction mode for one test (debug ABI), then back to auto."""
+    from paper_2605_26444_b200 import _native as N
+
+    def set_mode(m):
+        N.check(N.lib().nanospec_debug_set_head_mode(m), "nanospec_debug_set_head_mode")
+
+    yield set_mode
+    set_mode(-1)
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("n,k,m", [(60, 10, 3072), (1, 32, 3072), (60, 10, 129), (33, 7, 2500), (4, 10, 1)])
+def test_tc_reduction_modes(cuda_ok, llama, head_mode, mode, n, k, m):
+    """Each split-K reduction / top-k hand-off of the fused tensor-core head
+    (persistent finishers, L2 hand-off, DSMEM clusters) against the oracle."""
+    W, Wb = llama
+    head_mode(mode)
+    rng = np.random.default_rng(7 * n + m)
+    ids = rng.choice(W.shape[0], size=m, replace=False)
+    st = _state_with_ids(W.shape[0], ids, w_max=3072)
+    H = SI.bf16_hidden(n, W.shape[1], seed=n + m + 1, device="cuda")
+    _full_check(st, W, Wb, H, k, "tc", f"mode {mode} n={n} k={k} |I|={m}")
+    # repeated calls reuse the scratch (hand-off words must be left clean)
+    _full_check(st, W, Wb, H, k, "tc", f"mode {mode} repeat")
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_tc_modes_bit_exact(cuda_ok, head_mode, mode):
+    """Integer-valued operands: every mode gives bit-exact logits and ids."""
+    head_mode(mode)
+    V, d = 20000, 4096
+    W = SI.int_valued_bf16((V, d), -16, 16, seed=3, device="cuda")
+    Wb = SI.bf16_bits(W)
+    ids = np.random.default_rng(2).choice(V, size=3000, replace=False)
+    st = _state_with_ids(V, ids, w_max=3072)
+    H = SI.int_valued_bf16((60, d), -16, 16, seed=4, device="cuda")
+    _full_check(st, W, Wb, H, 10, "tc", f"integer-valued mode {mode}", exact=True)
+
+
+def test_large_active_set(cuda_ok, llama):
+    """A 16k window with ~11k active ids (the vp32k regime on one GPU): more
+    than 32 row tiles per sequence, so the automatic mode is the L2 hand-off."""
+    W, Wb = llama
+    rng = np.random.default_rng(11)
+    ids = rng.choice(W.shape[0], size=11000, replace=False)
+    st = _state_with_ids(W.shape[0], ids, w_max=16384)
+    H = SI.bf16_hidden(60, W.shape[1], seed=12, device="cuda")
+    _full_check(st, W, Wb, H, 10, "tc", "|I|=11000")
