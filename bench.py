@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--rotate", type=int, default=24, help="sequences with disjoint id pools (cold L2)")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-fuse", action="store_true", help="step = update + head as two launches")
     ap.add_argument("--cpu-sample-steps", type=int, default=3)
     return ap.parse_args()
 
@@ -217,7 +218,7 @@ def run_ours(args):
     R = max(1, min(R, V // pool))
     W = SI.bf16_weights(V, d, seed=0, device=dev)
     pools = SI.disjoint_pools(V, pool, R, seed=3 + rank)
-    total_steps_per_seq = (args.warmup + 2 * args.steps + 2 * R) // R + 4
+    total_steps_per_seq = (args.warmup + 3 * args.steps + 2 * R) // R + 6  # step, two-launch step, update-only, e2e
     states, outs, upd_d, upd_v = [], [], [], []
     Hs = SI.bf16_hidden(n, d, seed=1 + rank, device=dev, batch=R)
     for r in range(R):
@@ -230,12 +231,23 @@ def run_ours(args):
         upd_v.append(torch.as_tensor(np.stack([u[1] for u in ups]), device=dev))
     cursor = [0] * R
 
-    def step(s):
+    fused = (not args.no_fuse and args.head in ("auto", "tc")
+             and P.step_is_fused(states[0], 60, 3, d, n, k))
+
+    def step_unfused(s):
         r = s % R
         c = cursor[r]
         cursor[r] += 1
         states[r].update(0, upd_d[r][c], upd_v[r][c])
         P.draft_logits_topk(states[r], W, Hs[r:r + 1], k, impl=args.head, out=outs[r])
+
+    def step_fused(s):
+        r = s % R
+        c = cursor[r]
+        cursor[r] += 1
+        P.step(states[r], 0, upd_d[r][c], upd_v[r][c], W, Hs[r], k, out=outs[r])
+
+    step = step_fused if fused else step_unfused
 
     def head_only(s):
         r = s % R
@@ -288,6 +300,14 @@ def run_ours(args):
     us_step = ms_total * 1e3 / K
     us_head = statistics.median(head_ms) * 1e3
 
+    # the same step as two launches (update, then head), for the breakdown
+    g_unf = capture(step_unfused, K, 0)
+    ev0.record(stream)
+    g_unf.replay()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    us_step_unfused = ev0.elapsed_time(ev1) * 1e3 / K
+
     # state update alone (its own graph over the next fresh updates)
     def upd_only(s):
         r = s % R
@@ -323,8 +343,11 @@ def run_ours(args):
         Hd.copy_(Hh, non_blocking=True)
         ud_d.copy_(ud_h[r][c], non_blocking=True)
         uv_d.copy_(uv_h[r][c], non_blocking=True)
-        states[r].update(0, ud_d, uv_d)
-        tl, ti, ts, _ = P.draft_logits_topk(states[r], W, Hd, k, impl=args.head, out=outs[r])
+        if fused:
+            tl, ti, ts = P.step(states[r], 0, ud_d, uv_d, W, Hd[0], k, out=outs[r])
+        else:
+            states[r].update(0, ud_d, uv_d)
+            tl, ti, ts, _ = P.draft_logits_topk(states[r], W, Hd, k, impl=args.head, out=outs[r])
         out_l.copy_(tl[0], non_blocking=True)
         out_i.copy_(ti[0], non_blocking=True)
         out_s.copy_(ts[0], non_blocking=True)
@@ -379,14 +402,18 @@ def run_ours(args):
         with open(tpath) as f:
             traffic = json.load(f).get("traffic_bytes")
     alg_bytes = Wm * d * 2 + n * d * 2 + Wm * 4 + n * k * 8 + n * 4
-    achieved = alg_bytes / (us_head * 1e-6) / 1e9
+    # the dominant kernel: the fused step kernel (one launch per step: update +
+    # gather + contraction + top-k); unfused, the head kernel
+    us_kernel = us_step if fused else us_head
+    achieved = alg_bytes / (us_kernel * 1e-6) / 1e9
+    achieved_head = alg_bytes / (us_head * 1e-6) / 1e9
 
     cpu = None
     if rank == 0 and not args.no_cpu:
         us_cpu, sample = cpu_oracle_steps(cfg, n, k, args.cpu_sample_steps)
         cpu = {"value": round(us_cpu, 1), "unit": "us/step", "cores": 1, "kind": "oracle", "sample": sample}
 
-    launches_per_step = 3 if args.head == "simt" else 2  # state update + fused head (SIMT: + select)
+    launches_per_step = 1 if fused else (3 if args.head == "simt" else 2)  # fused step | update + head (+ select)
     value = ms_total * 1e3 / (K * world)
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "us/step", "n_gpus": world, "steps": K,
@@ -397,12 +424,15 @@ def run_ours(args):
                    "l2": f"inputs larger than L2: {R} rotating sequences with disjoint id pools "
                          f"({R * Wm * d * 2 / 1e6:.0f} MB of distinct rows > 126 MB L2)",
                    "parallelism": f"dp{world} (independent sequences, no collective)",
-                   "step": "state_update(60 draft + 3 verify ids) + draft_logits_topk"},
-        "breakdown": {"us_step": round(us_step, 3), "us_head_call": round(us_head, 3),
-                      "us_state_update": round(us_upd, 3), "head_gbps": round(achieved, 1)},
+                   "step": ("nanospec_step: state update (60 draft + 3 verify ids) fused with the head, one launch"
+                            if fused else "state_update(60 draft + 3 verify ids) + draft_logits_topk")},
+        "breakdown": {"us_step": round(us_step, 3), "fused": bool(fused),
+                      "us_step_two_launches": round(us_step_unfused, 3), "us_head_call": round(us_head, 3),
+                      "us_state_update": round(us_upd, 3), "head_only_gbps": round(achieved_head, 1)},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "draft_logits_topk call (contraction + top-k select)",
+                     "kernel": ("fused step kernel (update + gather + contraction + top-k), per launch" if fused
+                                else "draft_logits_topk call (contraction + top-k select)"),
                      "alg_bytes_per_launch": alg_bytes},
         "dense": {kk: (round(vv, 3) if isinstance(vv, float) else vv) for kk, vv in dense.items()},
         "cpu_baseline": cpu,

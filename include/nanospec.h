@@ -210,6 +210,31 @@ nanospec_status nanospec_merge_topk(const float* d_cand_logit, const int32_t* d_
                                     int32_t n_shards, int32_t n_rows, int32_t k, float* d_out_logit,
                                     int32_t* d_out_id, float* d_out_lse, cudaStream_t stream);
 
+/* One decode step of sequence `seq` in ONE launch where possible: the state
+ * update (Eq. 4 + Eq. 5; exactly nanospec_state_update) followed by
+ * the restricted head over the UPDATED active set (Eq. 2 on I, P:205;
+ * SelectDraftTokens P:527-528; exactly nanospec_draft_logits_topk on that
+ * sequence).  The fused kernel streams the rows of the pre-update slots while
+ * one CTA applies the update, then adds the entering ids as patch tiles and
+ * drops the rows whose id left I, so the update is off the critical path.
+ * Shapes it cannot fuse (rule R2, lists > 512 ids, large windows, clusters
+ * that do not fit one wave) run as two launches with identical results.
+ *   d_draft_ids int32[n_draft], d_verify_topk int32[k_ver]  (as state_update)
+ *   d_hidden    bf16 [n_nodes x d_model] (this sequence's tree nodes)
+ *   d_topk_logit / d_topk_id [n_nodes x k], d_lse [n_nodes] or NULL
+ *   d_scratch  >= nanospec_head_scratch_bytes(1, w_max, n_nodes), zeroed once.
+ * Errors as nanospec_state_update + nanospec_draft_logits_topk. */
+nanospec_status nanospec_step(nanospec_state st, int32_t seq, const int32_t* d_draft_ids, int32_t n_draft,
+                              const int32_t* d_verify_topk, int32_t k_ver, const void* d_w_head, int32_t d_model,
+                              int64_t ldw, const void* d_hidden, int32_t n_nodes, int32_t k, float* d_topk_logit,
+                              int32_t* d_topk_id, float* d_lse, void* d_scratch, size_t scratch_bytes,
+                              cudaStream_t stream);
+
+/* 1 if nanospec_step with these sizes runs as ONE fused launch on the current
+ * device, 0 if it runs as update + head (same results).  Host-only query. */
+int32_t nanospec_step_fused(const nanospec_state st, int32_t n_draft, int32_t k_ver, int32_t d_model,
+                            int32_t n_nodes, int32_t k);
+
 /* Debug: phase trace.  d_buf = device uint64[ctas * 16] (ctas >= 256) or NULL
  * (off, the default).  While set, the fused tensor-core head writes the
  * %globaltimer (ns) of its phases, CTA b at d_buf[b*16 + e]: 0 start,
@@ -225,6 +250,10 @@ nanospec_status nanospec_debug_set_trace(unsigned long long* d_buf, int32_t ctas
  * (poll), 2 clusters of K-split CTAs with DSMEM reduction.  A forced mode the
  * shape cannot use falls back to the automatic choice.  Process-wide; tests. */
 nanospec_status nanospec_debug_set_head_mode(int32_t mode);
+
+/* Debug: cap the thread-block-cluster size (K splits per row tile, 2..8) the
+ * cluster-mode head and the fused step try; 0 = no cap (default).  Tests. */
+nanospec_status nanospec_debug_set_cluster_cap(int32_t s);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

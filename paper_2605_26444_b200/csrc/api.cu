@@ -9,6 +9,7 @@
 #include "nanospec.h"
 #include "common.cuh"
 #include "internal.h"
+#include "state_fast.cuh"
 
 using namespace nanospec;
 
@@ -290,6 +291,73 @@ nanospec_status nanospec_draft_logits_topk(const nanospec_state st, const void* 
                                        d_lse, d_debug_logits, d_scratch, scratch_bytes, NANOSPEC_HEAD_AUTO, stream);
 }
 
+nanospec_status nanospec_step(nanospec_state st, int32_t seq, const int32_t* d_draft_ids, int32_t n_draft,
+                              const int32_t* d_verify_topk, int32_t k_ver, const void* d_w_head, int32_t d_model,
+                              int64_t ldw, const void* d_hidden, int32_t n_nodes, int32_t k, float* d_topk_logit,
+                              int32_t* d_topk_id, float* d_lse, void* d_scratch, size_t scratch_bytes,
+                              cudaStream_t stream) {
+  if (!st || seq < 0 || seq >= st->sv.batch || n_draft < 0 || k_ver < 0) return NANOSPEC_EINVAL;
+  if ((n_draft > 0 && !d_draft_ids) || (k_ver > 0 && !d_verify_topk)) return NANOSPEC_EINVAL;
+  if (!d_w_head || !d_hidden || !d_topk_logit || !d_topk_id) return NANOSPEC_EINVAL;
+  if (d_model <= 0 || d_model % 8 != 0 || ldw < d_model || ldw % 8 != 0) return NANOSPEC_EINVAL;
+  if (n_nodes < 1 || n_nodes > NANOSPEC_MAX_NODES || k < 1 || k > NANOSPEC_MAX_K) return NANOSPEC_EINVAL;
+  if (!aligned16(d_w_head) || !aligned16(d_hidden)) return NANOSPEC_EINVAL;
+  const StateView& sv = st->sv;
+  if (!d_scratch || scratch_bytes < nanospec_head_scratch_bytes(1, sv.w_max, n_nodes)) return NANOSPEC_EINVAL;
+  HeadProblem hp;
+  hp.w = (const uint16_t*)d_w_head;
+  hp.ldw = ldw;
+  hp.d = d_model;
+  hp.h = (const uint16_t*)d_hidden;
+  hp.n = n_nodes;
+  hp.batch = 1;
+  hp.ids_base = sv.ids + (size_t)seq * sv.w_max;
+  hp.ids_stride = sv.w_max;
+  hp.nact_base = &sv.meta[seq].n_active;
+  hp.nact_stride = sizeof(Meta) / sizeof(int32_t);
+  hp.max_ids = sv.w_max;
+  hp.n_shards = sv.n_shards;
+  hp.logits = nullptr;
+  hp.trace = trace_buffer();
+  if (state_fast_path(sv, 0, d_draft_ids ? n_draft : 0, 1, d_verify_topk ? k_ver : 0, 1)) {
+    AppendArgs upd;
+    upd.sv = sv;
+    upd.seq0 = seq;
+    upd.reset = 0;
+    upd.a = ListArg{d_draft_ids, d_draft_ids ? n_draft : 0, 0, 1};
+    upd.b = ListArg{d_verify_topk, d_verify_topk ? k_ver : 0, 0, 1};
+    const size_t lb = logits_bytes(1, sv.w_max, n_nodes);
+    cudaError_t e = launch_step_tc(hp, upd, k, d_topk_logit, d_topk_id, d_lse, (char*)d_scratch + lb,
+                                   scratch_bytes - lb, sm_count(), stream);
+    if (e == cudaSuccess) return NANOSPEC_OK;
+    if (e != cudaErrorNotSupported) return NANOSPEC_ECUDA;
+  }
+  // not fusable: the update, then the head on that sequence (two launches)
+  nanospec_status r = nanospec_state_update(st, seq, d_draft_ids, n_draft, d_verify_topk, k_ver, stream);
+  if (r != NANOSPEC_OK) return r;
+  return run_head(hp, k, d_topk_logit, d_topk_id, d_lse, nullptr, d_scratch, scratch_bytes, NANOSPEC_HEAD_AUTO,
+                  stream);
+}
+
+int32_t nanospec_step_fused(const nanospec_state st, int32_t n_draft, int32_t k_ver, int32_t d_model,
+                            int32_t n_nodes, int32_t k) {
+  if (!st || n_draft < 0 || k_ver < 0 || d_model <= 0 || d_model % 8 != 0) return 0;
+  if (n_nodes < 1 || n_nodes > NANOSPEC_MAX_NODES || k < 1 || k > NANOSPEC_MAX_K) return 0;
+  const StateView& sv = st->sv;
+  if (!state_fast_path(sv, 0, n_draft, 1, k_ver, 1)) return 0;
+  HeadProblem hp = {};
+  hp.d = d_model;
+  hp.ldw = d_model;
+  hp.n = n_nodes;
+  hp.batch = 1;
+  hp.max_ids = sv.w_max;
+  AppendArgs upd = {};
+  upd.sv = sv;
+  upd.a.len = n_draft;
+  upd.b.len = k_ver;
+  return launch_step_tc(hp, upd, k, nullptr, nullptr, nullptr, nullptr, 0, sm_count(), 0, true) == cudaSuccess ? 1 : 0;
+}
+
 nanospec_status nanospec_logits_topk_ids(const int32_t* d_ids, const int32_t* d_n_ids, int32_t max_ids,
                                          int32_t n_shards, const void* d_w_head, int32_t d_model, int64_t ldw,
                                          const void* d_hidden, int32_t n_nodes, int32_t k, float* d_topk_logit,
@@ -328,6 +396,12 @@ nanospec_status nanospec_debug_set_trace(unsigned long long* d_buf, int32_t ctas
 nanospec_status nanospec_debug_set_head_mode(int32_t mode) {
   if (mode < -1 || mode > 2) return NANOSPEC_EINVAL;
   set_head_tc_mode(mode);
+  return NANOSPEC_OK;
+}
+
+nanospec_status nanospec_debug_set_cluster_cap(int32_t s) {
+  if (s < 0 || s > 8) return NANOSPEC_EINVAL;
+  set_head_tc_cluster_cap(s);
   return NANOSPEC_OK;
 }
 

@@ -38,6 +38,7 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "state_fast.cuh"
 
 namespace nanospec {
 
@@ -65,6 +66,7 @@ constexpr uint32_t kEncG = 0x7fffffffu;  // list ids: valid ids are < 2^31 - 1, 
 constexpr int kModeFinish = 0;   // persistent CTAs, grid barrier, one finisher CTA per (sequence, node)
 constexpr int kModePoll = 1;     // one unit per CTA, split-K partials + lists handed over through L2
 constexpr int kModeCluster = 2;  // one unit per CTA, the S splits of a tile form a cluster (DSMEM reduction)
+constexpr int kModeFused = 3;    // cluster mode + the state update in the same launch (patch tiles)
 constexpr int kMaxCluster = 8;   // portable cluster size
 constexpr int kMaxL2Lists = 160;  // poll mode: tiles per sequence (5 lists per lane at level 2)
 constexpr long long kSpinLimit = 1ll << 26;  // polls before giving up (a trap beats a hung GPU)
@@ -74,7 +76,16 @@ struct TcArgs {
   unsigned* grid_word;  // grid barrier: (generation << kCountBits) | arrivals
   float* part;          // [tiles_g * S][n][128] partial tiles (split-K partials, or whole tiles for S = 1)
   uint2* cand;          // poll mode: [tiles_g][n][k + 1] level-1 lists (+ lse partial), encoded
-  int mode;             // kModeCluster / kModePoll / kModeFinish (see the launcher)
+  int mode;             // kModeCluster / kModePoll / kModeFinish / kModeFused (see the launchers)
+  // fused update + head (kModeFused): one sequence, its update and its head in one launch
+  AppendArgs upd;       // the state update (fast path) of sequence upd.seq0
+  unsigned* step_ctr;   // publication generation of the update's results
+  unsigned* arrive_ctr; // CTAs that have read the pre-update ids / n_active
+  uint32_t* stale;      // [w_max / 32] slots (pre-update) whose id left I
+  int32_t* enter_ids;   // [kFastThreads] global ids entering I
+  int* enter_meta;      // {ne, n_new}
+  int tps_reg;          // row tiles over the pre-update slots; patch tiles follow
+  int n_patch;          // patch tiles (distinct update-list ids, 128 per tile); then the update cluster
   unsigned* node_ctr;   // cluster mode: [batch * n] level-1 arrivals per (sequence, node); zero between launches
   float* topk_logit;    // [batch][n][k]
   int32_t* topk_id;
@@ -460,7 +471,7 @@ __device__ __forceinline__ uint2 warp_topk_thr(const uint32_t (&key)[4], const u
 // (the caller's release atomic orders them).
 template <bool kPollMode>
 __device__ void level1(const TcArgs& a, int tile, int node, const int32_t* ids_s, int rows, int row0,
-                       const float* Pm, uint2* scratch) {
+                       const float* Pm, uint2* scratch, uint32_t stale4 = 0u) {
   const HeadProblem& p = a.p;
   const int lane = threadIdx.x & 31;
   const int S = a.S, k = a.k;
@@ -510,7 +521,7 @@ __device__ void level1(const TcArgs& a, int tile, int node, const int32_t* ids_s
     uint32_t lmk = 0u;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const bool ok = r0 + i < rows;
+      const bool ok = r0 + i < rows && !((stale4 >> i) & 1u);  // fused step: rows whose id left I
       key[i] = ok ? float_key(v[i]) : 0u;
       gid[i] = ok ? (uint32_t)ids_s[r0 + i] : 0xffffffffu;
       lmk = key[i] > lmk ? key[i] : lmk;
@@ -704,11 +715,15 @@ __device__ void poll_tail(const TcArgs& a, int tile, int split, const int32_t* i
 // t's head and lse partial in one round trip; T = k-th largest head (k lists
 // each own an entry >= T); every list's entries >= T (its sorted prefix) are
 // compacted into the warp scratch and ranked by counting.
-__device__ void level2_thr(const TcArgs& a, int seq, int node, int ntiles, uint2* scratch) {
+// List t comes from tile t (t < nreg), else from tile treg + t - nreg (the
+// fused step's patch tiles).
+__device__ void level2_thr(const TcArgs& a, int seq, int node, int ntiles, uint2* scratch, int nreg = 1 << 30,
+                           int treg = 0) {
   const HeadProblem& p = a.p;
   const int lane = threadIdx.x & 31;
   const int k = a.k, kl = k + 1;
-  const uint2* lst = a.cand + ((long long)(seq * a.tps + lane) * p.n + node) * kl;
+  const int lt = lane < nreg ? lane : treg + lane - nreg;
+  const uint2* lst = a.cand + ((long long)(seq * a.tps + lt) * p.n + node) * kl;
   uint2 head = make_uint2(0u, 0xffffffffu), st = make_uint2(__float_as_uint(-INFINITY), 0u);
   if (lane < ntiles) { head = __ldcg(lst); st = __ldcg(lst + k); }
   float bm = __uint_as_float(st.x), be = __uint_as_float(st.y);
@@ -734,9 +749,8 @@ __device__ void level2_thr(const TcArgs& a, int seq, int node, int ntiles, uint2
       any = any || bal;
     }
     if (!__any_sync(0xffffffffu, any)) break;  // lists are sorted: nothing further qualifies
-    if (cnt + 32 * 8 > 1024) break;            // (cannot happen: <= k lists reach past T's rank)
   }
-  uint2* best = scratch + 1024;
+  uint2* best = scratch + ntiles * k;  // cnt <= ntiles * k; the launcher sized the warp scratch for ntiles * (k + 1)
   if (lane < k) best[lane] = make_uint2(0u, 0xffffffffu);
   __syncwarp();
   warp_rank_write(scratch, cnt, k, best);
@@ -777,13 +791,147 @@ __device__ void cluster_tail(const TcArgs& a, int tile, int split, const int32_t
       if (last) a.node_ctr[seq * p.n + c] = 0u;  // every tile has arrived: reset for the next launch
     }
     last = __shfl_sync(0xffffffffu, last, 0);
-    if (last) {  // the launcher picks cluster mode only for <= 32 tiles per sequence
-      if ((smem_bytes - pbytes) / 8 / kWarps >= 1024 + kMaxK) level2_thr(a, seq, c, ntiles, scratch);
-      else level2<1, false>(a, seq, c, ntiles, scratch);
-    }
+    if (last) level2_thr(a, seq, c, ntiles, scratch);  // cluster mode: <= 32 tiles per sequence
   }
   if (threadIdx.x == 0) trace_mark(p.trace, 10);
   cluster_sync();  // peers are done reading this CTA's partial tile
+}
+
+// ---------------------------------------------------------------- fused step
+// The update's hand-off to the head, run by every thread of the updating CTA
+// between the count update and the slot-table writes: the stale-slot bitmap
+// (pre-update slots whose id left I) and the entering ids go to scratch; once
+// every other CTA has read the pre-update ids / n_active (arrive counter) the
+// generation is bumped (release) and update_fast goes on to rewrite ids[].
+struct FusedPublish {
+  const TcArgs* a;
+  uint32_t* stale_s;  // shared, w_max / 32 words
+  __device__ void operator()(const StateView& sv, UpdSmem& sm, int n_old, int nl, int ne) const {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int words = (sv.w_max + 31) >> 5;
+    for (int w = tid; w < words; w += nt) stale_s[w] = 0u;
+    __syncthreads();
+    for (int q = tid; q < nl; q += nt) atomicOr(&stale_s[sm.hole[q] >> 5], 1u << (sm.hole[q] & 31));
+    __syncthreads();
+    for (int w = tid; w < words; w += nt) a->stale[w] = stale_s[w];
+    const int32_t gmul = sv.n_shards <= 1 ? 1 : sv.n_shards, gadd = sv.n_shards <= 1 ? 0 : sv.rank;
+    for (int t = tid; t < ne; t += nt) a->enter_ids[t] = sm.enter[t] * gmul + gadd;
+    if (tid == 0) { a->enter_meta[0] = ne; a->enter_meta[1] = n_old - nl + ne; a->enter_meta[2] = n_old; }
+    __syncthreads();
+    if (tid == 0) {
+      long long spins = 0;
+      trace_mark(a->p.trace, 13);  // updater: counts done, waiting for the readers
+      while (ld_acquire(a->arrive_ctr) != gridDim.x - 1u)
+        if (++spins > kSpinLimit) __trap();
+      *a->arrive_ctr = 0u;  // every arrival of this launch is in
+      __threadfence();
+      red_add_release(a->step_ctr, 1u);
+    }
+    __syncthreads();
+  }
+};
+
+__device__ __forceinline__ void wait_published(const TcArgs& a, unsigned g0) {
+  if (threadIdx.x == 0) {
+    long long spins = 0;
+    while (ld_acquire(a.step_ctr) == g0)
+      if (++spins > kSpinLimit) __trap();
+  }
+  __syncthreads();
+}
+
+// Distinct valid ids of the update lists (draft, then verify), first
+// occurrence, computed identically by every patch CTA; ids_s[t] = the
+// (base + t)-th of them.  Returns their count.  `sm`: 2 * kHashSlots +
+// kFastThreads + 64 ints of scratch shared memory.
+__device__ int fused_unique_ids(const TcArgs& a, int32_t* sm, int base, int32_t* ids_s) {
+  int32_t* hkey = sm;
+  int32_t* hval = sm + kHashSlots;
+  int32_t* uniq = sm + 2 * kHashSlots;
+  int* scan = reinterpret_cast<int*>(uniq + kFastThreads);
+  const int tid = threadIdx.x;
+  const StateView& sv = a.upd.sv;
+  const int la = (int)a.upd.a.len, lb = (int)a.upd.b.len, L = la + lb;
+  for (int h = tid; h < kHashSlots; h += blockDim.x) { hkey[h] = -1; hval[h] = 0x7fffffff; }
+  int32_t e = -1;
+  if (tid < la) e = a.upd.a.ptr[tid];
+  else if (tid < L) e = a.upd.b.ptr[tid - la];
+  __syncthreads();
+  const bool valid = tid < L && e >= 0 && e < sv.vocab && is_local(sv, e);
+  int hs = -1;
+  if (valid) {
+    hs = hash_insert(hkey, e);
+    atomicMin(&hval[hs], tid);
+  }
+  __syncthreads();
+  const bool keep = valid && hval[hs] == tid;
+  int nu;
+  const int pos = block_exclusive_scan(keep ? 1 : 0, scan, &nu);
+  if (keep) uniq[pos] = e;
+  __syncthreads();
+  if (tid < kBM) ids_s[tid] = base + tid < nu ? uniq[base + tid] : 0;
+  __syncthreads();
+  return nu;
+}
+
+__device__ __forceinline__ bool hash_contains(const int32_t* keys, int32_t key) {
+  int h = hash_slot(key);
+  while (true) {
+    const int32_t k2 = keys[h];
+    if (k2 == key) return true;
+    if (k2 == -1) return false;
+    h = (h + 1) & (kHashSlots - 1);
+  }
+}
+
+// Tail of a fused-step CTA (cluster mode), after the update has published:
+// regular tiles drop the rows whose id left I (stale slots), patch tiles keep
+// only the rows of ids entering I (a shared-memory hash of the published
+// entering ids); level 2 merges the lists of the nreg live regular tiles and
+// all n_patch patch tiles.  The last 8 KB of the stage area hold the hash.
+__device__ void fused_tail(const TcArgs& a, int tile, int split, const int32_t* ids_s, int nu, const float* Pm,
+                           uint2* smem, int smem_bytes) {
+  const HeadProblem& p = a.p;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = a.S;
+  const bool patch = tile >= a.tps_reg;
+  const int m_old = __ldcg(&a.enter_meta[2]);
+  const int nreg = (m_old + kBM - 1) / kBM;
+  const int ntiles = nreg + a.n_patch;
+  const int row0 = patch ? (tile - a.tps_reg) * kBM : tile * kBM;
+  const int rows = min(kBM, (patch ? nu : m_old) - row0);
+  const int hash_bytes = kHashSlots * 4;
+  int32_t* hkey = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(smem) + smem_bytes - hash_bytes);
+  uint32_t drop4 = 0u;  // this lane's rows (4 * lane + i) that do not count
+  if (!patch) {
+    drop4 = (__ldcg(&a.stale[(row0 >> 5) + (lane >> 3)]) >> ((lane & 7) * 4)) & 0xfu;
+  } else {
+    const int ne = __ldcg(&a.enter_meta[0]);
+    for (int h = threadIdx.x; h < kHashSlots; h += blockDim.x) hkey[h] = -1;
+    __syncthreads();
+    for (int t = threadIdx.x; t < ne; t += blockDim.x) hash_insert(hkey, __ldcg(&a.enter_ids[t]));
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (4 * lane + i < rows && !hash_contains(hkey, ids_s[4 * lane + i])) drop4 |= 1u << i;
+  }
+  cluster_sync();  // every CTA of the cluster has its partial tile in shared memory
+  if (threadIdx.x == 0) trace_mark(p.trace, 5);
+  const int pbytes = (p.n * kBM * 4 + 1023) / 1024 * 1024;
+  uint2* scratch = smem + pbytes / 8 + (long long)warp * ((smem_bytes - hash_bytes - pbytes) / 8 / kWarps);
+  for (int c = split + S * warp; c < p.n; c += S * kWarps) {
+    level1<false>(a, tile, c, ids_s, rows, row0, Pm, scratch, drop4);
+    __syncwarp();
+    unsigned last = 0;
+    if (lane == 0) {
+      last = atom_add_acq_rel(&a.node_ctr[c], 1u) == (unsigned)(ntiles - 1);
+      if (last) a.node_ctr[c] = 0u;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) level2_thr(a, 0, c, ntiles, scratch, nreg, a.tps_reg);
+  }
+  if (threadIdx.x == 0) trace_mark(p.trace, 10);
+  cluster_sync();
 }
 
 template <int NT, int MODE>  // one instantiation per mode: only its own tail is compiled in
@@ -827,6 +975,8 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
   // launched now; it waits for this grid's completion before touching state
   asm volatile("griddepcontrol.launch_dependents;");
   if (tid == 0) trace_mark(p.trace, 1);  // dependency resolved
+  __shared__ unsigned sh_g0;
+  if (MODE == kModeFused && tid == 0) sh_g0 = ld_acquire(a.step_ctr);  // before anyone can publish
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -843,19 +993,55 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
   const int step = S > 1 ? tiles_g : (int)gridDim.x;
   int it = 0;      // pipeline iteration counter across units
   int local = 0;   // units processed by this CTA
+  bool patch_rows = false;
+  if (MODE == kModeFused && first == a.tps_reg + a.n_patch) {
+    // the update cluster: CTA 0 applies the state update (its dependent global
+    // round trips overlap the streaming of every other cluster), the others
+    // just check in; none of them streams
+    if (split == 0) {
+      FusedPublish pub{&a, reinterpret_cast<uint32_t*>(smem + (sizeof(UpdSmem) + 255) / 256 * 256)};
+      update_fast(a.upd, a.upd.seq0, *reinterpret_cast<UpdSmem*>(smem), pub, nullptr);
+      if (tid == 0) trace_mark(p.trace, 11);  // updater: state updated and published
+    } else if (tid == 0) {
+      red_add_release(a.arrive_ctr, 1u);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == kLoadWarps) {
+      tc_fence_after();
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::kTmemCols));
+    }
+    return;
+  }
   for (int tile = first; tile < tiles_g; tile += step) {
     const int seq = tile / a.tps, tin = tile - (tile / a.tps) * a.tps;
-    const int row0 = tin * kBM;
-    // one round trip: the tile's ids (rows past n_active are never dereferenced)
-    // and n_active
-    if (tid < kBM) ids_s[tid] = row0 + tid < p.max_ids ? __ldcg(p.ids_base + (long long)seq * p.ids_stride + row0 + tid) : 0;
-    if (tid == kBM) sh_m = clamp_nact(p, seq);
-    __syncthreads();
+    int row0 = tin * kBM;
+    int m;
+    if (MODE == kModeFused && tile >= a.tps_reg) {
+      // patch tile p: rows [128p, 128p + 128) of the distinct valid ids of the
+      // update lists (draft, then verify; first occurrence) -- a superset of the
+      // ids entering I, known without waiting for the update; the rows of ids
+      // that were already active are dropped at level 1
+      if (tid == 0) red_add_release(a.arrive_ctr, 1u);
+      const int nu = fused_unique_ids(a, reinterpret_cast<int32_t*>(smem), (tile - a.tps_reg) * kBM, ids_s);
+      row0 = (tile - a.tps_reg) * kBM;
+      m = nu;
+      if (tid == 0) sh_m = nu;
+      patch_rows = true;
+    } else {
+      // one round trip: the tile's ids (rows past n_active are never dereferenced)
+      // and n_active
+      if (tid < kBM) ids_s[tid] = row0 + tid < p.max_ids ? __ldcg(p.ids_base + (long long)seq * p.ids_stride + row0 + tid) : 0;
+      if (tid == kBM) sh_m = clamp_nact(p, seq);
+      __syncthreads();
+      if (MODE == kModeFused && tid == 0) red_add_release(a.arrive_ctr, 1u);  // pre-update ids / n_active read
+      m = sh_m;
+    }
     if (tid == 0 && local == 0) trace_mark(p.trace, 7);  // ids + n_active in shared memory
-    const int m = sh_m;
     const int rows = min(kBM, m - row0);
     if (rows <= 0) {  // past n_active: every CTA of the tile skips it
       __syncthreads();
+      if (MODE == kModeFused && patch_rows) local = -1;  // fused: the empty patch tile still publishes padding
       continue;
     }
     const int kb0 = split * KB / S, kb1 = (split + 1) * KB / S;
@@ -908,7 +1094,7 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
       const int r = lg * 32 + lane;               // TMEM lane == tile row
       const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16);
       // per column, the 32 lanes of a warp store 128 consecutive bytes
-      float* Pw = MODE == kModeCluster ? reinterpret_cast<float*>(smem) + r
+      float* Pw = (MODE == kModeCluster || MODE == kModeFused) ? reinterpret_cast<float*>(smem) + r
                                          : a.part + (((long long)tile * S + split) * p.n) * kBM + r;
       if (cgp < C::kColGroups) {
 #pragma unroll 1
@@ -964,6 +1150,15 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::kTmemCols));
   }
   if (tid == 0) trace_mark(p.trace, 9);  // drained
+  if (MODE == kModeFused) {
+    wait_published(a, sh_g0);
+    if (tid == 0) trace_mark(p.trace, 12);  // publication seen
+    if (local != 0)
+      fused_tail(a, first, split, ids_s, local < 0 ? 0 : sh_m, reinterpret_cast<const float*>(smem),
+                 reinterpret_cast<uint2*>(smem), C::kStageArea);
+    if (tid == 0) trace_mark(p.trace, 8);  // done
+    return;
+  }
   if (MODE == kModeCluster) {
     if (local > 0)
       cluster_tail(a, first, split, ids_s, sh_m, reinterpret_cast<const float*>(smem), reinterpret_cast<uint2*>(smem),
@@ -1008,10 +1203,20 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
 }
 
 int g_head_mode = -1;  // -1 auto; kModeFinish / kModePoll / kModeCluster forced where feasible
+int g_cluster_cap = 0;
+// The fused step is launched WITHOUT programmatic dependent launch: its CTAs
+// wait on each other across clusters (arrivals, publication), which needs the
+// whole grid resident; an early-launched dependent grid places its clusters on
+// the SMs this grid frees and can fragment the GPCs so that some of its own
+// clusters cannot be placed while its placed CTAs wait for them (measured:
+// graph of 200 back-to-back steps faulted with PDL, passes without).  The
+// head-only kernels have no cross-cluster waits and keep PDL.
+int g_fused_pdl = 0;  // debug: largest cluster (K-split) size tried, 0 = kMaxCluster
 
 struct ScratchLayout {
-  size_t grid_word, node_ctr, part, cand, total;
+  size_t grid_word, node_ctr, part, cand, step_ctr, arrive_ctr, stale, enter_ids, enter_meta, total;
 };
+constexpr int kMaxPatchTiles = kFastThreads / kBM;  // fused step: entering ids <= kFastThreads
 
 // S * tiles_g <= kMaxSMs whenever S > 1, and S = 1 otherwise: the partial
 // buffer holds max(kMaxSMs, tiles) tiles of n x 128 floats.
@@ -1023,8 +1228,13 @@ inline ScratchLayout scratch_layout(int batch, int max_ids, int n) {
   L.grid_word = off; off += al(sizeof(unsigned));
   L.node_ctr = off;  off += al(sizeof(unsigned) * (size_t)batch * n);
   L.part = off;      off += al((tiles > (size_t)kMaxSMs ? tiles : (size_t)kMaxSMs) * n * kBM * sizeof(float));
-  const size_t ctiles = tiles < (size_t)kMaxSMs ? tiles : (size_t)kMaxSMs;  // poll mode: tiles_g <= #SMs
+  const size_t ctiles = (tiles < (size_t)kMaxSMs ? tiles : (size_t)kMaxSMs) + kMaxPatchTiles;
   L.cand = off;      off += al(ctiles * n * (kMaxK + 1) * sizeof(uint2));
+  L.step_ctr = off;  off += al(sizeof(unsigned));
+  L.arrive_ctr = off; off += al(sizeof(unsigned));
+  L.stale = off;     off += al(sizeof(uint32_t) * (size_t)((max_ids + 31) / 32));
+  L.enter_ids = off; off += al(sizeof(int32_t) * kFastThreads);
+  L.enter_meta = off; off += al(sizeof(int) * 4);
   L.total = off;
   return L;
 }
@@ -1054,6 +1264,13 @@ cudaError_t launch_nt(const HeadProblem& p, int k, float* topk_logit, int32_t* t
   a.part = (float*)(sc + L.part);
   a.cand = (uint2*)(sc + L.cand);
   a.node_ctr = (unsigned*)(sc + L.node_ctr);
+  a.step_ctr = (unsigned*)(sc + L.step_ctr);
+  a.arrive_ctr = (unsigned*)(sc + L.arrive_ctr);
+  a.stale = (uint32_t*)(sc + L.stale);
+  a.enter_ids = (int32_t*)(sc + L.enter_ids);
+  a.enter_meta = (int*)(sc + L.enter_meta);
+  a.tps_reg = 0;
+  a.n_patch = 0;
   a.topk_logit = topk_logit;
   a.topk_id = topk_id;
   a.lse = lse;
@@ -1070,7 +1287,8 @@ cudaError_t launch_nt(const HeadProblem& p, int k, float* topk_logit, int32_t* t
   const int env_mode = g_head_mode;  // debug override (nanospec_debug_set_head_mode), -1 = auto
   int S = 1, mode = kModeFinish;
   if (tiles_g <= G && a.tps <= kMaxL2Lists && (long long)a.tps * (k + 1) * 8 <= (C::kStageArea - p.n * kBM * 4 - 1024) / kWarps) {
-    for (int s = kMaxCluster; s >= 2 && a.tps <= 32 && env_mode != kModePoll && env_mode != kModeFinish; --s) {
+    const int smax = g_cluster_cap >= 2 && g_cluster_cap < kMaxCluster ? g_cluster_cap : kMaxCluster;
+    for (int s = smax; s >= 2 && a.tps <= 32 && env_mode != kModePoll && env_mode != kModeFinish; --s) {
       if (s > KB || s * tiles_g > G) continue;
       if (max_clusters[s] == 0) {
         cudaLaunchConfig_t q = {};
@@ -1135,11 +1353,133 @@ cudaError_t launch_nt(const HeadProblem& p, int k, float* topk_logit, int32_t* t
   return e;
 }
 
+// Fused step: the state update of one sequence (fast path) and its head in
+// one launch.  Clusters of S K-split CTAs over the tps_reg row tiles of the
+// pre-update slots plus P patch tiles for the entering ids; CTA 0 of the first
+// patch cluster runs the update.  cudaErrorNotSupported when the clusters do
+// not all fit in one wave (the caller then launches update + head).
+template <int NT>
+cudaError_t launch_step_nt(const HeadProblem& p, const AppendArgs& upd, int k, float* topk_logit, int32_t* topk_id,
+                           float* lse, void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t stream,
+                           bool dry_run) {
+  using C = Cfg<NT>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e =
+        cudaFuncSetAttribute(head_tc_kernel<NT, kModeFused>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const ScratchLayout L = scratch_layout(1, p.max_ids, p.n);
+  if (!dry_run && L.total > scratch_bytes) return cudaErrorInvalidValue;
+  const int G = num_sms < kMaxSMs ? num_sms : kMaxSMs;
+  const int KB = p.d / kBK;
+  const int tps_reg = (p.max_ids + kBM - 1) / kBM;
+  const long long nl = upd.a.len + upd.b.len;
+  const int P = nl <= 0 ? 1 : (int)((nl + kBM - 1) / kBM);  // patch tiles
+  const int tiles_g = tps_reg + P + 1;                         // + the update cluster
+  if (P > kMaxPatchTiles || tps_reg + P > 32 || tiles_g * 2 > G) return cudaErrorNotSupported;
+  if ((long long)((sizeof(UpdSmem) + 255) / 256 * 256) + (p.max_ids + 31) / 32 * 4 > C::kStageArea)
+    return cudaErrorNotSupported;
+  const long long warp_entries = (C::kStageArea - kHashSlots * 4 - (p.n * kBM * 4 + 1023) / 1024 * 1024) / 8 / kWarps;
+  if ((long long)(tps_reg + P) * (k + 1) > warp_entries || warp_entries < kBM) return cudaErrorNotSupported;
+  static int max_clusters[kMaxCluster + 1] = {0};
+  int S = 0;
+  const int smax = g_cluster_cap >= 2 && g_cluster_cap < kMaxCluster ? g_cluster_cap : kMaxCluster;
+  for (int s = smax; s >= 2; --s) {
+    if (s > KB || s * tiles_g > G) continue;
+    if (max_clusters[s] == 0) {
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(s * tiles_g);
+      q.blockDim = dim3(kThreads);
+      q.dynamicSmemBytes = C::kSmemBytes;
+      cudaLaunchAttribute ca;
+      ca.id = cudaLaunchAttributeClusterDimension;
+      ca.val.clusterDim.x = s;
+      ca.val.clusterDim.y = 1;
+      ca.val.clusterDim.z = 1;
+      q.attrs = &ca;
+      q.numAttrs = 1;
+      int nc = 0;
+      if (cudaOccupancyMaxActiveClusters(&nc, head_tc_kernel<NT, kModeFused>, &q) != cudaSuccess || nc <= 0) {
+        (void)cudaGetLastError();
+        nc = -1;
+      }
+      max_clusters[s] = nc;
+    }
+    if (max_clusters[s] >= tiles_g) { S = s; break; }
+  }
+  if (S < 2) return cudaErrorNotSupported;
+  if (dry_run) return cudaSuccess;
+  char* sc = (char*)scratch;
+  TcArgs a;
+  a.p = p;
+  a.grid_word = (unsigned*)(sc + L.grid_word);
+  a.part = (float*)(sc + L.part);
+  a.cand = (uint2*)(sc + L.cand);
+  a.node_ctr = (unsigned*)(sc + L.node_ctr);
+  a.step_ctr = (unsigned*)(sc + L.step_ctr);
+  a.arrive_ctr = (unsigned*)(sc + L.arrive_ctr);
+  a.stale = (uint32_t*)(sc + L.stale);
+  a.enter_ids = (int32_t*)(sc + L.enter_ids);
+  a.enter_meta = (int*)(sc + L.enter_meta);
+  a.upd = upd;
+  a.topk_logit = topk_logit;
+  a.topk_id = topk_id;
+  a.lse = lse;
+  a.k = k;
+  a.tps = tiles_g;
+  a.tps_reg = tps_reg;
+  a.n_patch = P;
+  a.S = S;
+  a.mode = kModeFused;
+
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(tiles_g * S);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::kSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attrs[2];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  attrs[1].id = cudaLaunchAttributeClusterDimension;
+  attrs[1].val.clusterDim.x = S;
+  attrs[1].val.clusterDim.y = 1;
+  attrs[1].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 2;
+  if (g_fused_pdl == 0) { cfg.attrs = attrs + 1; cfg.numAttrs = 1; }
+  cudaError_t e = cudaLaunchKernelEx(&cfg, head_tc_kernel<NT, kModeFused>, a);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    cfg.attrs = attrs + 1;  // without PDL
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, head_tc_kernel<NT, kModeFused>, a);
+  }
+  return e;
+}
+
 }  // namespace
 
 size_t head_tc_scratch_bytes(int batch, int max_ids, int n) { return scratch_layout(batch, max_ids, n).total; }
 
 void set_head_tc_mode(int mode) { g_head_mode = mode; }
+void set_head_tc_cluster_cap(int s) { g_cluster_cap = s; }
+
+cudaError_t launch_step_tc(const HeadProblem& p, const AppendArgs& upd, int k, float* topk_logit, int32_t* topk_id,
+                           float* lse, void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t stream,
+                           bool dry_run) {
+  if (p.batch != 1 || p.d % kBK != 0 || p.n < 1 || p.n > 256 || p.ldw % 8 != 0 || k < 1 || k > kMaxK)
+    return cudaErrorNotSupported;
+#define NS_STEP(NTV) \
+  launch_step_nt<NTV>(p, upd, k, topk_logit, topk_id, lse, scratch, scratch_bytes, num_sms, stream, dry_run)
+  if (p.n <= 16) return NS_STEP(16);
+  if (p.n <= 32) return NS_STEP(32);
+  if (p.n <= 64) return NS_STEP(64);
+  if (p.n <= 128) return NS_STEP(128);
+  return NS_STEP(256);
+#undef NS_STEP
+}
 
 cudaError_t launch_head_tc(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse,
                            void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t stream) {

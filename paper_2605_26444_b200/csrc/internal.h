@@ -42,8 +42,20 @@ cudaError_t launch_head_simt(const HeadProblem& p, int num_sms, cudaStream_t str
 cudaError_t launch_head_tc(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse,
                            void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t stream);
 size_t head_tc_scratch_bytes(int batch, int max_ids, int n);
+struct AppendArgs;
+// Fused step: the fast-path update `upd` (one sequence, rule R1) and the head of
+// that sequence in one launch (p.batch == 1, p points at that sequence).
+// cudaErrorNotSupported when the shape cannot be fused (caller: update + head).
+// dry_run: only decide (cudaSuccess = would fuse), launch nothing.
+cudaError_t launch_step_tc(const HeadProblem& p, const AppendArgs& upd, int k, float* topk_logit, int32_t* topk_id,
+                           float* lse, void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t stream,
+                           bool dry_run = false);
+// Whether launch_state_append would take the per-step fast path for these lists.
+bool state_fast_path(const StateView& sv, int reset, long long a_len, int a_dedup, long long b_len, int b_dedup);
 // Debug: force the fused head's reduction mode (-1 auto, 0 finisher, 1 poll, 2 cluster).
 void set_head_tc_mode(int mode);
+// Debug: cap the cluster (K-split) size the cluster / fused modes try (0 = no cap).
+void set_head_tc_cluster_cap(int s);
 
 // Phase 2 (a5): per (sequence, node) top-k by (value desc, id asc) + lse.
 cudaError_t launch_select_topk(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse,

@@ -184,6 +184,35 @@ def draft_logits_topk(state: ActiveVocab, w_head: torch.Tensor, hidden: torch.Te
     return out.topk_logit, out.topk_id, out.lse, out.debug_logits
 
 
+def step(state: ActiveVocab, seq: int, draft: torch.Tensor | None, verify: torch.Tensor | None,
+         w_head: torch.Tensor, hidden: torch.Tensor, k: int, *, lse: bool = True, out: HeadOutputs | None = None):
+    """One decode step of sequence `seq`: the state update (Eq. 4/5) and the head
+    over the updated active set, fused into one launch when the
+    shape allows (nanospec_step).  hidden: bf16 [n_nodes, d].
+    Returns (topk_logit [1,n,k], topk_id [1,n,k], lse [1,n] or None)."""
+    _need(w_head, torch.bfloat16, "w_head")
+    _need(hidden, torch.bfloat16, "hidden")
+    d = w_head.shape[-1]
+    n_nodes = hidden.numel() // d
+    for t, name in ((draft, "draft"), (verify, "verify")):
+        if t is not None:
+            _need(t, torch.int32, name)
+    if out is None:
+        out = HeadOutputs(1, n_nodes, k, state.w_max, hidden.device, lse, False)
+    st = N.lib().nanospec_step(
+        state.handle, seq, _ptr(draft), 0 if draft is None else draft.numel(), _ptr(verify),
+        0 if verify is None else verify.numel(), _ptr(w_head), d, w_head.stride(0), _ptr(hidden), n_nodes, k,
+        _ptr(out.topk_logit), _ptr(out.topk_id), _ptr(out.lse), _ptr(out.scratch), out.scratch.numel(),
+        _stream(hidden.device))
+    N.check(st, "nanospec_step")
+    return out.topk_logit, out.topk_id, out.lse
+
+
+def step_is_fused(state: ActiveVocab, n_draft: int, k_ver: int, d_model: int, n_nodes: int, k: int) -> bool:
+    """Whether step() with these sizes runs as one fused launch on this device."""
+    return bool(N.lib().nanospec_step_fused(state.handle, n_draft, k_ver, d_model, n_nodes, k))
+
+
 def logits_topk_ids(ids: torch.Tensor, n_ids: torch.Tensor, w_head: torch.Tensor, hidden: torch.Tensor, k: int, *,
                     n_shards: int = 1, lse: bool = True, debug_logits: bool = False, impl: str = "auto",
                     out: HeadOutputs | None = None):

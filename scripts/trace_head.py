@@ -16,7 +16,8 @@ from paper_2605_26444_b200 import _native as N  # noqa: E402
 from synthetic import inputs as SI  # noqa: E402
 
 EVENTS = ["start", "dep_ok", "rowptr", "loads_landed", "mma_done", "fin_go", "-", "ids_ready",
-          "done", "drained", "l1|fin_staged", "l2|fin_summed", "l2staged|fin_warp_topk", "l1_all|fin_lists"]
+          "done", "drained", "l1|fin_staged", "l2|fin_summed|upd_done", "l2staged|fin_warp_topk|pub_seen",
+          "l1_all|fin_lists|upd_counts"]
 
 
 def main():
@@ -25,12 +26,17 @@ def main():
     ap.add_argument("--m", type=int, default=3072)
     ap.add_argument("--k", type=int, default=10)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--step", action="store_true", help="trace the fused step (update + head) instead")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     V, d = 128256, 4096
     W = SI.bf16_weights(V, d, seed=0, device=dev)
     ids = np.random.default_rng(0).choice(V, args.m, replace=False).astype(np.int32)
     st = P.ActiveVocab(V, 3072 if args.m <= 3072 else args.m, device=dev)
+    if args.step:  # headline recipe: |I| = W_max, 63 fresh ids per step
+        pool = SI.disjoint_pools(V, st.w_max + 126, 1, seed=5)[0]
+        ids, ups = SI.cyclic_fresh_updates(pool, st.w_max, 4 * args.reps + 4)
+        upd_iter = iter([(torch.as_tensor(a, device=dev), torch.as_tensor(b, device=dev)) for a, b in ups])
     st.init(0, torch.as_tensor(ids, device=dev))
     H = SI.bf16_hidden(args.n, d, seed=1, device=dev).reshape(1, args.n, d)
     out = P.HeadOutputs(1, args.n, args.k, st.w_max, dev)
@@ -49,7 +55,11 @@ def main():
             N.check(N.lib().nanospec_debug_set_trace(trace.data_ptr(), 256), "set_trace")
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            P.draft_logits_topk(st, W, H, args.k, impl="tc", out=out)
+            if args.step:
+                dd, vv = next(upd_iter)
+                P.step(st, 0, dd, vv, W, H[0], args.k, out=out)
+            else:
+                P.draft_logits_topk(st, W, H, args.k, impl="tc", out=out)
             e1.record()
             torch.cuda.synchronize()
             N.check(N.lib().nanospec_debug_set_trace(None, 0), "set_trace")

@@ -1,0 +1,200 @@
+"""The fused decode step (nanospec_step: state update + head in one launch,
+P:229-239 then P:527-528) against the oracle: after every step the state is
+bit-exact (ids, n_active, bitmap, ring, total) and the top-k / lse of the
+UPDATED active set pass the parity rules.  Covers the headline regime (|I| =
+W_max, 63 ids enter and 63 leave per step), natural Zipf streams (I grows and
+shrinks, duplicates inside the lists, ids already active), invalid ids, and
+shapes that fall back to two launches."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from synthetic import inputs as SI
+
+from parity import check_lse, check_topk
+
+pytestmark = pytest.mark.gpu
+
+
+def _t(a):
+    return torch.as_tensor(np.asarray(a, np.int32), dtype=torch.int32, device="cuda").contiguous()
+
+
+def _check_state(st, ref, what):
+    got = st.read(0)
+    ids, bm = ref.active()
+    assert got["n_active"] == len(ids), what
+    assert np.array_equal(got["ids"], ids), what
+    assert np.array_equal(got["bitmap"], bm), what
+    ring, total = ref.ring()
+    assert got["total"] == total and np.array_equal(got["ring"], ring), what
+    return ids
+
+
+def _check_head(v, i, l, ids, Wb, H, k, what):
+    z_ref, A = O.logits(Wb, SI.bf16_bits(H), ids)
+    v_ref, id_ref = O.topk(z_ref, ids, k)
+    check_topk(v[0].cpu().numpy(), i[0].cpu().numpy(), z_ref, A, ids, v_ref, id_ref, what)
+    check_lse(l[0].cpu().numpy(), O.lse(z_ref), what)
+
+
+@pytest.fixture(scope="module")
+def llama():
+    W = SI.bf16_weights(SI.LLAMA["vocab"], SI.LLAMA["d_model"], seed=0, device="cuda")
+    return W, SI.bf16_bits(W)
+
+
+def test_step_headline_regime(cuda_ok, llama):
+    """|I| = W_max = 3072 every step: 63 fresh ids enter, 63 leave."""
+    from paper_2605_26444_b200 import ActiveVocab, HeadOutputs, step
+    W, Wb = llama
+    V, d = W.shape
+    Wm, n, k = 3072, 60, 10
+    pool = SI.disjoint_pools(V, Wm + 126, 1, seed=5)[0]
+    prompt, ups = SI.cyclic_fresh_updates(pool, Wm, 6)
+    st = ActiveVocab(V, Wm)
+    st.init(0, _t(prompt))
+    ref = O.OracleStream(V, Wm).init(prompt)
+    out = HeadOutputs(1, n, k, Wm, "cuda")
+    for s, (dd, vv) in enumerate(ups):
+        H = SI.bf16_hidden(n, d, seed=100 + s, device="cuda")
+        v, i, l = step(st, 0, _t(dd), _t(vv), W, H, k, out=out)
+        torch.cuda.synchronize()
+        ref.update(dd, vv)
+        ids = _check_state(st, ref, f"step {s}")
+        assert len(ids) == Wm
+        _check_head(v, i, l, ids, Wb, H, k, f"headline step {s}")
+
+
+@pytest.mark.parametrize("n,k", [(60, 10), (10, 3), (1, 32)])
+def test_step_natural_stream(cuda_ok, llama, n, k):
+    """Zipf stream: repeated and already-active ids, I shrinking and growing."""
+    from paper_2605_26444_b200 import ActiveVocab, HeadOutputs, step
+    W, Wb = llama
+    V, d = W.shape
+    Wm = 3072
+    z = SI.Zipf(V)
+    prompt, pre = SI.prompt_and_prefill(z, 3, 600, 3)
+    st = ActiveVocab(V, Wm)
+    st.init(0, _t(prompt), _t(pre))
+    ref = O.OracleStream(V, Wm).init(prompt, pre)
+    out = HeadOutputs(1, n, k, Wm, "cuda")
+    for s, (dd, vv) in enumerate(SI.decode_steps(z, 9, 60)):
+        H = SI.bf16_hidden(n, d, seed=200 + s, device="cuda")
+        v, i, l = step(st, 0, _t(dd), _t(vv), W, H, k, out=out)
+        ref.update(dd, vv)
+        if s % 6 == 5 or s < 2:
+            torch.cuda.synchronize()
+            ids = _check_state(st, ref, f"zipf step {s}")
+            _check_head(v, i, l, ids, Wb, H, k, f"zipf n={n} k={k} step {s}")
+
+
+def test_step_small_window_and_invalid_ids(cuda_ok, llama):
+    """W_max = 256 (evictions every step), out-of-range ids (dropped, flagged)."""
+    from paper_2605_26444_b200 import ActiveVocab, HeadOutputs, step
+    W, Wb = llama
+    V, d = W.shape
+    Wm, n, k = 256, 16, 10
+    rng = np.random.default_rng(4)
+    st = ActiveVocab(V, Wm)
+    prompt = rng.integers(0, V, 300)
+    st.init(0, _t(prompt))
+    ref = O.OracleStream(V, Wm).init(prompt)
+    out = HeadOutputs(1, n, k, Wm, "cuda")
+    for s in range(12):
+        dd = rng.integers(0, V, 60)
+        dd[::7] = dd[1]  # duplicates within the list
+        if s == 5:
+            dd[3] = V + 5  # invalid: dropped
+        vv = rng.integers(0, V, 3)
+        H = SI.bf16_hidden(n, d, seed=300 + s, device="cuda")
+        v, i, l = step(st, 0, _t(dd), _t(vv), W, H, k, out=out)
+        torch.cuda.synchronize()
+        ref.update(dd, vv)
+        ids = _check_state(st, ref, f"small-window step {s}")
+        _check_head(v, i, l, ids, Wb, H, k, f"small-window step {s}")
+    assert st.check() != 0  # the invalid id was flagged
+
+
+def test_step_fallback_tiny(cuda_ok):
+    """A shape the fused kernel does not take (d = 64: one K block, no split)
+    runs as update + head with the same results."""
+    from paper_2605_26444_b200 import ActiveVocab, step
+    V, d, Wm, n, k = 1000, 64, 256, 8, 10
+    W = SI.bf16_weights(V, d, seed=0, device="cuda")
+    Wb = SI.bf16_bits(W)
+    z = SI.Zipf(V)
+    prompt, pre = SI.prompt_and_prefill(z, 2, 200, 3)
+    st = ActiveVocab(V, Wm)
+    st.init(0, _t(prompt), _t(pre))
+    ref = O.OracleStream(V, Wm).init(prompt, pre)
+    for s, (dd, vv) in enumerate(SI.decode_steps(z, 5, 5, n_draft=8, k_ver=3)):
+        H = SI.bf16_hidden(n, d, seed=1 + s, device="cuda")
+        v, i, l = step(st, 0, _t(dd), _t(vv), W, H, k)
+        torch.cuda.synchronize()
+        ref.update(dd, vv)
+        ids = _check_state(st, ref, f"tiny step {s}")
+        _check_head(v, i, l, ids, Wb, H, k, f"tiny step {s}")
+
+
+@pytest.mark.parametrize("cap", [2, 3, 4, 6])
+def test_step_cluster_sizes(cuda_ok, llama, cap):
+    """The fused step with the cluster (K-split) size capped: every split count
+    gives the oracle's state and top-k."""
+    from paper_2605_26444_b200 import ActiveVocab, HeadOutputs, step, _native as N
+    W, Wb = llama
+    V, d = W.shape
+    Wm, n, k = 3072, 60, 10
+    N.check(N.lib().nanospec_debug_set_cluster_cap(cap), "cluster cap")
+    try:
+        z = SI.Zipf(V)
+        prompt, pre = SI.prompt_and_prefill(z, 8, 1500, 3)
+        st = ActiveVocab(V, Wm)
+        st.init(0, _t(prompt), _t(pre))
+        ref = O.OracleStream(V, Wm).init(prompt, pre)
+        out = HeadOutputs(1, n, k, Wm, "cuda")
+        for s, (dd, vv) in enumerate(SI.decode_steps(z, 13, 4)):
+            H = SI.bf16_hidden(n, d, seed=400 + s, device="cuda")
+            v, i, l = step(st, 0, _t(dd), _t(vv), W, H, k, out=out)
+            torch.cuda.synchronize()
+            ref.update(dd, vv)
+            ids = _check_state(st, ref, f"cap {cap} step {s}")
+            _check_head(v, i, l, ids, Wb, H, k, f"cap {cap} step {s}")
+    finally:
+        N.check(N.lib().nanospec_debug_set_cluster_cap(0), "cluster cap")
+
+
+def test_step_many_back_to_back(cuda_ok, llama):
+    """200 fused steps over 8 sequences captured in one CUDA graph (programmatic
+    dependent launch between them), then every sequence checked."""
+    from paper_2605_26444_b200 import ActiveVocab, HeadOutputs, step
+    W, Wb = llama
+    V, d = W.shape
+    Wm, n, k, R, T = 3072, 60, 10, 8, 200
+    pools = SI.disjoint_pools(V, Wm + 126, R, seed=9)
+    sts, outs, refs, ups, Hs = [], [], [], [], SI.bf16_hidden(n, d, seed=7, device="cuda", batch=R)
+    for r in range(R):
+        prompt, u = SI.cyclic_fresh_updates(pools[r], Wm, T // R + 2)
+        st = ActiveVocab(V, Wm)
+        st.init(0, _t(prompt))
+        sts.append(st)
+        refs.append(O.OracleStream(V, Wm).init(prompt))
+        outs.append(HeadOutputs(1, n, k, Wm, "cuda"))
+        ups.append([(_t(a), _t(b), a, b) for a, b in u])
+    stream = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for s in range(T):
+            r = s % R
+            dd, vv, _, _ = ups[r][s // R]
+            step(sts[r], 0, dd, vv, W, Hs[r], k, out=outs[r])
+    g.replay()
+    torch.cuda.synchronize()
+    for r in range(R):
+        for j in range(T // R):
+            refs[r].update(ups[r][j][2], ups[r][j][3])
+        ids = _check_state(sts[r], refs[r], f"seq {r}")
+        v, i, l = outs[r].topk_logit, outs[r].topk_id, outs[r].lse
+        _check_head(v, i, l, ids, Wb, Hs[r], k, f"graph seq {r}")
