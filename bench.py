@@ -323,6 +323,38 @@ def run_ours(args):
     torch.cuda.synchronize()
     us_upd = ev0.elapsed_time(ev1) * 1e3 / U
 
+    # SURVEY 8(d) extras: warm L2 (the same active set again, as within one draft
+    # round), narrower trees (n = 1, 10), and a draft round of one n = 1 call +
+    # five n = 10 calls on one active set (the shape of the paper's T4 step)
+    def timed(fn, count):
+        g = capture(fn, count, 0)
+        ev0.record(stream)
+        g.replay()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        return ev0.elapsed_time(ev1) * 1e3 / count
+
+    extra = {}
+    extra["us_head_warm_l2"] = timed(
+        lambda s: P.draft_logits_topk(states[0], W, Hs[0:1], k, impl=args.head, out=outs[0]), K)
+    hn = {}
+    for nn in (1, 10):
+        Hn = SI.bf16_hidden(nn, d, seed=50 + nn, device=dev, batch=R)
+        on = [P.HeadOutputs(1, nn, k, Wm, dev) for _ in range(R)]
+        hn[nn] = (Hn, on)
+        extra[f"us_head_n{nn}"] = timed(
+            lambda s, Hn=Hn, on=on: P.draft_logits_topk(states[s % R], W, Hn[s % R:s % R + 1], k, impl=args.head,
+                                                        out=on[s % R]), K)
+
+    def draft_round(s):
+        r = s % R
+        P.draft_logits_topk(states[r], W, hn[1][0][r:r + 1], k, impl=args.head, out=hn[1][1][r])
+        for _ in range(5):
+            P.draft_logits_topk(states[r], W, hn[10][0][r:r + 1], k, impl=args.head, out=hn[10][1][r])
+
+    extra["us_draft_round_1x1_5x10"] = timed(draft_round, max(R, K // 6))
+    extra = {kk: round(vv, 3) for kk, vv in extra.items()}
+
     # e2e through the public API with host buffers: H2D hidden + update ids, D2H top-k + lse
     Hh = Hs[0].cpu().pin_memory()
     ud_h = [upd_d[r].cpu().pin_memory() for r in range(R)]
@@ -391,6 +423,20 @@ def run_ours(args):
         ev1.record(stream)
         torch.cuda.synchronize()
         dense["ours_full_vocab_us"] = ev0.elapsed_time(ev1) * 1e3 / reps
+        # FR-Spec-shaped comparator: a fixed 32k-id set through the same kernel
+        fr_ids = torch.as_tensor(np.sort(np.random.default_rng(11).permutation(V)[:32768]).astype(np.int32),
+                                 device=dev)
+        fr_n = torch.tensor([32768], dtype=torch.int32, device=dev)
+        o_fr = P.HeadOutputs(1, n, k, 32768, dev)
+        for _ in range(3):
+            P.logits_topk_ids(fr_ids, fr_n, W, Hd1, k, impl=args.head, out=o_fr)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(reps):
+            P.logits_topk_ids(fr_ids, fr_n, W, Hd1, k, impl=args.head, out=o_fr)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        dense["ours_static_32k_set_us"] = ev0.elapsed_time(ev1) * 1e3 / reps
         dense["best_dense_us"] = min(dense["cublas_topk_us"], dense["ours_full_vocab_us"])
         dense["speedup_vs_dense"] = dense["best_dense_us"] / us_head
 
@@ -428,7 +474,7 @@ def run_ours(args):
                             if fused else "state_update(60 draft + 3 verify ids) + draft_logits_topk")},
         "breakdown": {"us_step": round(us_step, 3), "fused": bool(fused),
                       "us_step_two_launches": round(us_step_unfused, 3), "us_head_call": round(us_head, 3),
-                      "us_state_update": round(us_upd, 3), "head_only_gbps": round(achieved_head, 1)},
+                      "us_state_update": round(us_upd, 3), "head_only_gbps": round(achieved_head, 1), **extra},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                      "kernel": ("fused step kernel (update + gather + contraction + top-k), per launch" if fused

@@ -711,21 +711,32 @@ __device__ void poll_tail(const TcArgs& a, int tile, int split, const int32_t* i
   if (threadIdx.x == 0) trace_mark(p.trace, 11);  // warp 0: level 2 written
 }
 
-// Level 2 (cluster mode, lists complete) for ntiles <= 32: lane t fetches list
-// t's head and lse partial in one round trip; T = k-th largest head (k lists
-// each own an entry >= T); every list's entries >= T (its sorted prefix) are
-// compacted into the warp scratch and ranked by counting.
-// List t comes from tile t (t < nreg), else from tile treg + t - nreg (the
-// fused step's patch tiles).
+// Level 2 (cluster mode, lists complete) for ntiles <= 32, one global round
+// trip: lane t copies list t (k entries + its lse partial) into the warp's
+// scratch with 8-byte cp.async; T = k-th largest head (k lists each own an
+// entry >= T, so every top-k entry is >= T); each lane's sorted prefix >= T is
+// compacted (warp scan) and the candidates are ranked by counting.  Scratch:
+// ntiles * (2k + 1) + k entries.  List t comes from tile t (t < nreg), else
+// from tile treg + t - nreg (the fused step's patch tiles).
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
 __device__ void level2_thr(const TcArgs& a, int seq, int node, int ntiles, uint2* scratch, int nreg = 1 << 30,
                            int treg = 0) {
   const HeadProblem& p = a.p;
   const int lane = threadIdx.x & 31;
   const int k = a.k, kl = k + 1;
   const int lt = lane < nreg ? lane : treg + lane - nreg;
-  const uint2* lst = a.cand + ((long long)(seq * a.tps + lt) * p.n + node) * kl;
+  uint2* mine = scratch + lane * kl;
+  if (lane < ntiles) {
+    const uint2* lst = a.cand + ((long long)(seq * a.tps + lt) * p.n + node) * kl;
+    for (int j = 0; j < kl; ++j) cp_async8(smem_u32(mine + j), lst + j);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncwarp();
   uint2 head = make_uint2(0u, 0xffffffffu), st = make_uint2(__float_as_uint(-INFINITY), 0u);
-  if (lane < ntiles) { head = __ldcg(lst); st = __ldcg(lst + k); }
+  if (lane < ntiles) { head = mine[0]; st = mine[k]; }
   float bm = __uint_as_float(st.x), be = __uint_as_float(st.y);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -733,27 +744,22 @@ __device__ void level2_thr(const TcArgs& a, int seq, int node, int ntiles, uint2
     lse_fold(bm, be, m2, e2);
   }
   const uint32_t T = ntiles >= k ? warp_kth_key(head.x, k) : 0u;
-  int cnt = 0;
-  for (int j0 = 0; j0 < k; j0 += 8) {
-    uint2 e[8];
+  int c = 0;  // this lane's qualifying prefix
+  if (lane < ntiles)
+    while (c < k && mine[c].x != 0u && mine[c].x >= T) ++c;
+  int pre = c;  // inclusive warp scan
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      e[j] = (lane < ntiles && j0 + j < k) ? (j0 + j == 0 ? head : __ldcg(lst + j0 + j)) : make_uint2(0u, 0u);
-    bool any = false;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const bool c = e[j].x != 0u && e[j].x >= T;
-      const unsigned bal = __ballot_sync(0xffffffffu, c);
-      if (c) scratch[cnt + __popc(bal & ((1u << lane) - 1u))] = e[j];
-      cnt += __popc(bal);
-      any = any || bal;
-    }
-    if (!__any_sync(0xffffffffu, any)) break;  // lists are sorted: nothing further qualifies
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, pre, o);
+    if (lane >= o) pre += y;
   }
-  uint2* best = scratch + ntiles * k;  // cnt <= ntiles * k; the launcher sized the warp scratch for ntiles * (k + 1)
+  const int cnt = __shfl_sync(0xffffffffu, pre, 31);
+  uint2* cand = scratch + ntiles * kl;
+  for (int j = 0; j < c; ++j) cand[pre - c + j] = mine[j];
+  uint2* best = cand + ntiles * k;
   if (lane < k) best[lane] = make_uint2(0u, 0xffffffffu);
   __syncwarp();
-  warp_rank_write(scratch, cnt, k, best);
+  warp_rank_write(cand, cnt, k, best);
   __syncwarp();
   const long long ob = ((long long)seq * p.n + node) * k;
   if (lane < k) {
@@ -890,7 +896,7 @@ __device__ __forceinline__ bool hash_contains(const int32_t* keys, int32_t key) 
 // entering ids); level 2 merges the lists of the nreg live regular tiles and
 // all n_patch patch tiles.  The last 8 KB of the stage area hold the hash.
 __device__ void fused_tail(const TcArgs& a, int tile, int split, const int32_t* ids_s, int nu, const float* Pm,
-                           uint2* smem, int smem_bytes) {
+                           uint2* smem, int smem_bytes, const uint32_t* stale_tile) {
   const HeadProblem& p = a.p;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = a.S;
@@ -904,7 +910,7 @@ __device__ void fused_tail(const TcArgs& a, int tile, int split, const int32_t* 
   int32_t* hkey = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(smem) + smem_bytes - hash_bytes);
   uint32_t drop4 = 0u;  // this lane's rows (4 * lane + i) that do not count
   if (!patch) {
-    drop4 = (__ldcg(&a.stale[(row0 >> 5) + (lane >> 3)]) >> ((lane & 7) * 4)) & 0xfu;
+    drop4 = (stale_tile[lane >> 3] >> ((lane & 7) * 4)) & 0xfu;  // fetched by the MMA warp
   } else {
     const int ne = __ldcg(&a.enter_meta[0]);
     for (int h = threadIdx.x; h < kHashSlots; h += blockDim.x) hkey[h] = -1;
@@ -975,8 +981,10 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
   // launched now; it waits for this grid's completion before touching state
   asm volatile("griddepcontrol.launch_dependents;");
   if (tid == 0) trace_mark(p.trace, 1);  // dependency resolved
+  // fused: the publication generation each CTA waits past; read before the
+  // CTA arrives (the update publishes only after every arrival)
   __shared__ unsigned sh_g0;
-  if (MODE == kModeFused && tid == 0) sh_g0 = ld_acquire(a.step_ctr);  // before anyone can publish
+  __shared__ uint32_t sh_stale[kBM / 32];  // fused, regular tile: rows whose id left I
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -1022,7 +1030,10 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
       // update lists (draft, then verify; first occurrence) -- a superset of the
       // ids entering I, known without waiting for the update; the rows of ids
       // that were already active are dropped at level 1
-      if (tid == 0) red_add_release(a.arrive_ctr, 1u);
+      if (tid == 0) {
+        sh_g0 = ld_acquire(a.step_ctr);
+        red_add_release(a.arrive_ctr, 1u);
+      }
       const int nu = fused_unique_ids(a, reinterpret_cast<int32_t*>(smem), (tile - a.tps_reg) * kBM, ids_s);
       row0 = (tile - a.tps_reg) * kBM;
       m = nu;
@@ -1033,6 +1044,7 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
       // and n_active
       if (tid < kBM) ids_s[tid] = row0 + tid < p.max_ids ? __ldcg(p.ids_base + (long long)seq * p.ids_stride + row0 + tid) : 0;
       if (tid == kBM) sh_m = clamp_nact(p, seq);
+      if (MODE == kModeFused && tid == kBM + 1) sh_g0 = ld_acquire(a.step_ctr);  // same round trip
       __syncthreads();
       if (MODE == kModeFused && tid == 0) red_add_release(a.arrive_ctr, 1u);  // pre-update ids / n_active read
       m = sh_m;
@@ -1135,6 +1147,17 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
         }
         __syncwarp();
       }
+      if (MODE == kModeFused && !patch_rows) {
+        // meanwhile (drain in progress): the update's publication and this
+        // tile's stale-slot words, off the tail's critical path
+        if (lane == 0) {
+          long long spins = 0;
+          while (ld_acquire(a.step_ctr) == sh_g0)
+            if (++spins > kSpinLimit) __trap();
+        }
+        __syncwarp();
+        if (lane < kBM / 32) sh_stale[lane] = __ldcg(&a.stale[(row0 >> 5) + lane]);
+      }
       // the MMA warp waits until the epilogue has drained TMEM
       mbar_wait(smem_u32(&bars[2 * C::kStages + 1]), local & 1);
     }
@@ -1151,11 +1174,11 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
   }
   if (tid == 0) trace_mark(p.trace, 9);  // drained
   if (MODE == kModeFused) {
-    wait_published(a, sh_g0);
+    if (patch_rows || local == 0) wait_published(a, sh_g0);  // regular tiles: the MMA warp already did
     if (tid == 0) trace_mark(p.trace, 12);  // publication seen
     if (local != 0)
       fused_tail(a, first, split, ids_s, local < 0 ? 0 : sh_m, reinterpret_cast<const float*>(smem),
-                 reinterpret_cast<uint2*>(smem), C::kStageArea);
+                 reinterpret_cast<uint2*>(smem), C::kStageArea, sh_stale);
     if (tid == 0) trace_mark(p.trace, 8);  // done
     return;
   }
@@ -1286,9 +1309,11 @@ cudaError_t launch_nt(const HeadProblem& p, int k, float* topk_logit, int32_t* t
   static int max_clusters[kMaxCluster + 1] = {0};
   const int env_mode = g_head_mode;  // debug override (nanospec_debug_set_head_mode), -1 = auto
   int S = 1, mode = kModeFinish;
-  if (tiles_g <= G && a.tps <= kMaxL2Lists && (long long)a.tps * (k + 1) * 8 <= (C::kStageArea - p.n * kBM * 4 - 1024) / kWarps) {
+  const long long warp_bytes = (C::kStageArea - p.n * kBM * 4 - 1024) / kWarps;  // level-2 scratch per warp
+  if (tiles_g <= G && a.tps <= kMaxL2Lists && (long long)a.tps * (k + 1) * 8 <= warp_bytes) {
     const int smax = g_cluster_cap >= 2 && g_cluster_cap < kMaxCluster ? g_cluster_cap : kMaxCluster;
-    for (int s = smax; s >= 2 && a.tps <= 32 && env_mode != kModePoll && env_mode != kModeFinish; --s) {
+    const bool cl_ok = a.tps <= 32 && ((long long)a.tps * (2 * k + 1) + k) * 8 <= warp_bytes;
+    for (int s = smax; s >= 2 && cl_ok && env_mode != kModePoll && env_mode != kModeFinish; --s) {
       if (s > KB || s * tiles_g > G) continue;
       if (max_clusters[s] == 0) {
         cudaLaunchConfig_t q = {};
@@ -1382,7 +1407,7 @@ cudaError_t launch_step_nt(const HeadProblem& p, const AppendArgs& upd, int k, f
   if ((long long)((sizeof(UpdSmem) + 255) / 256 * 256) + (p.max_ids + 31) / 32 * 4 > C::kStageArea)
     return cudaErrorNotSupported;
   const long long warp_entries = (C::kStageArea - kHashSlots * 4 - (p.n * kBM * 4 + 1023) / 1024 * 1024) / 8 / kWarps;
-  if ((long long)(tps_reg + P) * (k + 1) > warp_entries || warp_entries < kBM) return cudaErrorNotSupported;
+  if ((long long)(tps_reg + P) * (2 * k + 1) + k > warp_entries || warp_entries < 2 * kBM) return cudaErrorNotSupported;
   static int max_clusters[kMaxCluster + 1] = {0};
   int S = 0;
   const int smax = g_cluster_cap >= 2 && g_cluster_cap < kMaxCluster ? g_cluster_cap : kMaxCluster;
