@@ -962,11 +962,11 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
   if (tid == 0 && p.trace) p.trace[(long long)blockIdx.x * kTraceSlots + 14] = clock64();
   if (tid == 0) {
     for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(smem_u32(&bars[s]), kLoaders);          // full: every loader thread arrives
+      mbar_init(smem_u32(&bars[s]), kLoadWarps);        // full: one arrival per loader warp
       mbar_init(smem_u32(&bars[C::kStages + s]), 1);    // empty: one tcgen05.commit
     }
     mbar_init(smem_u32(&bars[2 * C::kStages]), 1);              // tmem_full
-    mbar_init(smem_u32(&bars[2 * C::kStages + 1]), kLoaders);   // tmem_empty
+    mbar_init(smem_u32(&bars[2 * C::kStages + 1]), kLoadWarps);  // tmem_empty: one arrival per loader warp
     fence_proxy_async();
   }
   if (warp == kLoadWarps) {
@@ -1092,9 +1092,13 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
         }
         cp_async_commit();
         if (q >= C::kStages - 1) {
+          // this thread's copies of stage q - (kStages - 1) have landed; made
+          // visible to the tensor core's async proxy; one arrival per warp
+          // (512 per-thread shared-memory arrivals per stage were measurable)
           cp_async_wait<C::kStages - 1>();
           fence_proxy_async();
-          mbar_arrive(smem_u32(&bars[(it + q - (C::kStages - 1)) % C::kStages]));
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&bars[(it + q - (C::kStages - 1)) % C::kStages]));
         }
       }
       if (tid == 0 && local == 0) trace_mark(p.trace, 3);  // all loads issued and landed
@@ -1124,7 +1128,8 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
         }
       }
       tc_fence_before();
-      mbar_arrive(smem_u32(&bars[2 * C::kStages + 1]));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&bars[2 * C::kStages + 1]));
     } else {
       // ---------------- MMA issuer (warp 16, one lane)
       if (local > 0) {
