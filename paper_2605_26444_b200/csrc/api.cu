@@ -401,7 +401,7 @@ nanospec_status nanospec_debug_set_head_mode(int32_t mode) {
 
 nanospec_status nanospec_debug_set_cluster_cap(int32_t s) {
   if (s < 0 || s > 8) return NANOSPEC_EINVAL;
-  set_head_tc_cluster_cap(s);
+  set_head_tc_cluster_cap(s % 16);
   return NANOSPEC_OK;
 }
 

@@ -979,7 +979,9 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
   pdl_wait();
   // the next kernel on the stream (typically the next state update) may be
   // launched now; it waits for this grid's completion before touching state
-  asm volatile("griddepcontrol.launch_dependents;");
+  // the next kernel on the stream may be launched now (the fused step is
+  // launched without PDL; its trigger below is inert)
+  if (MODE != kModeFused) asm volatile("griddepcontrol.launch_dependents;");
   if (tid == 0) trace_mark(p.trace, 1);  // dependency resolved
   // fused: the publication generation each CTA waits past; read before the
   // CTA arrives (the update publishes only after every arrival)
@@ -1178,6 +1180,7 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::kTmemCols));
   }
   if (tid == 0) trace_mark(p.trace, 9);  // drained
+  if (MODE == kModeFused) asm volatile("griddepcontrol.launch_dependents;");  // late trigger
   if (MODE == kModeFused) {
     if (patch_rows || local == 0) wait_published(a, sh_g0);  // regular tiles: the MMA warp already did
     if (tid == 0) trace_mark(p.trace, 12);  // publication seen
@@ -1231,7 +1234,7 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
 }
 
 int g_head_mode = -1;  // -1 auto; kModeFinish / kModePoll / kModeCluster forced where feasible
-int g_cluster_cap = 0;
+int g_cluster_cap = 0;  // debug: largest cluster (K-split) size tried, 0 = kMaxCluster
 // The fused step is launched WITHOUT programmatic dependent launch: its CTAs
 // wait on each other across clusters (arrivals, publication), which needs the
 // whole grid resident; an early-launched dependent grid places its clusters on
@@ -1239,7 +1242,7 @@ int g_cluster_cap = 0;
 // clusters cannot be placed while its placed CTAs wait for them (measured:
 // graph of 200 back-to-back steps faulted with PDL, passes without).  The
 // head-only kernels have no cross-cluster waits and keep PDL.
-int g_fused_pdl = 0;  // debug: largest cluster (K-split) size tried, 0 = kMaxCluster
+int g_fused_pdl = 0;  // (PDL with the trigger moved after the stream also faulted: kept off)
 
 struct ScratchLayout {
   size_t grid_word, node_ctr, part, cand, step_ctr, arrive_ctr, stale, enter_ids, enter_meta, total;
