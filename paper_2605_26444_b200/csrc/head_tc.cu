@@ -1142,6 +1142,11 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
         const int g_it = it + q;
         const int stage = g_it % C::kStages;
         mbar_wait(smem_u32(&bars[stage]), (g_it / C::kStages) & 1);
+        if (MODE == kModeCluster && lane == 0 && local == 0 && p.trace) {  // debug trace: stage readiness
+          if (q == 0) trace_mark(p.trace, 11);
+          if (q == nk / 2) trace_mark(p.trace, 12);
+          if (q == nk - 1) trace_mark(p.trace, 13);
+        }
         tc_fence_after();
         if (lane == 0) {
           const uint32_t sA = smem_u32(smem + stage * C::kStageBytes);

@@ -16,8 +16,8 @@ from paper_2605_26444_b200 import _native as N  # noqa: E402
 from synthetic import inputs as SI  # noqa: E402
 
 EVENTS = ["start", "dep_ok", "rowptr", "loads_landed", "mma_done", "fin_go", "-", "ids_ready",
-          "done", "drained", "l1|fin_staged", "l2|fin_summed|upd_done", "l2staged|fin_warp_topk|pub_seen",
-          "l1_all|fin_lists|upd_counts"]
+          "done", "drained", "l1|fin_staged", "l2|fin_summed|upd_done|stage0_full", "l2staged|pub_seen|stage_mid_full",
+          "l1_all|upd_counts|stage_last_full"]
 
 
 def main():
