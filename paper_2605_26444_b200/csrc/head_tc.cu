@@ -483,11 +483,11 @@ __device__ void level1(const TcArgs& a, int tile, int node, const int32_t* ids_s
     for (int j0 = 0; j0 < S; j0 += 4) {
       float4 x[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (j0 + j < S) x[j] = ld_dsmem_v4(mapa_shared(la, (uint32_t)(j0 + j)));
+      for (int j = 0; j < 4; ++j)  // K chunk j of this tile was computed by cluster rank (j - tile) mod S
+        if (j0 + j < S) x[j] = ld_dsmem_v4(mapa_shared(la, (uint32_t)((j0 + j + S - tile % S) % S)));
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        if (j0 + j < S) { v[0] += x[j].x; v[1] += x[j].y; v[2] += x[j].z; v[3] += x[j].w; }  // split order
+        if (j0 + j < S) { v[0] += x[j].x; v[1] += x[j].y; v[2] += x[j].z; v[3] += x[j].w; }  // K-chunk order
     }
   }
   for (int s0 = 0; kPollMode && s0 < S; s0 += 8) {
@@ -1058,7 +1058,12 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
       if (MODE == kModeFused && patch_rows) local = -1;  // fused: the empty patch tile still publishes padding
       continue;
     }
-    const int kb0 = split * KB / S, kb1 = (split + 1) * KB / S;
+    // K chunk of this CTA: cluster modes rotate the chunk by the tile, so at any
+    // moment the 24 tiles' CTAs read S different slices of H instead of all
+    // hitting the same L2 lines (the reduction sums in chunk order, so equal
+    // rows in different tiles still give bit-equal logits)
+    const int chunk = (MODE == kModeCluster || MODE == kModeFused) ? (split + tile) % S : split;
+    const int kb0 = chunk * KB / S, kb1 = (chunk + 1) * KB / S;
     const int nk = kb1 - kb0;
 
     if (warp < kLoadWarps) {

@@ -62,6 +62,25 @@ __global__ void __launch_bounds__(kThreads, 1) gather_kernel(Args a, const __gri
     a.t[512 + blockIdx.x] = t0;
   }
   if (MODE == 9) {
+  } else if (MODE == 8) {
+    // K-split, M0's lane mapping (8 threads per 128-B row piece), every stage in flight at once
+    const int tile = blockIdx.x / a.S, split = blockIdx.x % a.S;
+    const int KB = D / 64, kb0 = split * KB / a.S, kb1 = (split + 1) * KB / a.S, nk = kb1 - kb0;
+    if (tid < 128) rid[tid] = a.ids[tile * 128 + tid];
+    __syncthreads();
+    const int lr = tid >> 3;
+    const int swz = ((tid & 7) ^ (lr & 7)) << 4;
+    const uint16_t* rp0 = a.w + (long long)rid[lr] * D + (tid & 7) * 8;
+    const uint16_t* rp1 = a.w + (long long)rid[lr + 64] * D + (tid & 7) * 8;
+    for (int q = 0; q < nk; ++q) {
+      const uint32_t st = sa(sm + q * 16384);
+      const int col = (kb0 + q) * 64;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(st + lr * 128 + swz), "l"(rp0 + col) : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(st + (lr + 64) * 128 + swz), "l"(rp1 + col) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    acc = reinterpret_cast<float*>(sm)[tid];
   } else if (MODE == 6 || MODE == 7) {
     // K-split, 128 rows x [kb0, kb1): M6 ring of 4 x 32 KB stages (256 B per row per stage,
     // 64 B contiguous per thread); M7 everything in flight at once (up to 13 K-blocks = 208 KB)
@@ -309,6 +328,7 @@ int main() {
       run("M0 cp.async k-split ring", gather_kernel<0>, 24 * S, 8 * 16384 + 1024, S, cold);
       run("M1 tma gather4 k-split ring", gather_kernel<1>, 24 * S, 8 * 16384 + 1024, S, cold);
     }
+    run("M8 cp.async k-split ALL in flight", gather_kernel<8>, 120, 13 * 16384 + 1024, 5, cold);
     run("M6 cp.async k-split ring4x32K", gather_kernel<6>, 120, 4 * 32768 + 1024, 5, cold);
     run("M7 cp.async k-split all-in-flight", gather_kernel<7>, 120, 7 * 32768 + 1024, 5, cold);
     run("M2 tma gather4 row-split", gather_kernel<2>, 148, 64 * 24 * 128 + 1024, 1, cold);
@@ -317,5 +337,12 @@ int main() {
     run("M5 cp.async row-split", gather_kernel<5>, 148, 21 * 8192 + 1024, 1, cold);
     if (!cold) break;
   }
+  // the same K-split gathers with every 3072-id set sorted ascending (the slot
+  // table's order after init): a 128-row tile then spans ~1/24 of the vocabulary
+  for (int r = 0; r < R; ++r) std::sort(perm.begin() + (size_t)r * M, perm.begin() + (size_t)(r + 1) * M);
+  cudaMemcpy(ids, perm.data(), (size_t)R * M * 4, cudaMemcpyHostToDevice);
+  run("M0 ring, SORTED ids", gather_kernel<0>, 120, 8 * 16384 + 1024, 5, true);
+  run("M8 all in flight, SORTED ids", gather_kernel<8>, 120, 13 * 16384 + 1024, 5, true);
+  run("M5 row-split, SORTED ids", gather_kernel<5>, 148, 21 * 8192 + 1024, 1, true);
   return 0;
 }
