@@ -437,6 +437,18 @@ def run_ours(args):
         ev1.record(stream)
         torch.cuda.synchronize()
         dense["ours_static_32k_set_us"] = ev0.elapsed_time(ev1) * 1e3 / reps
+        # verify side: T_Kver = top-3 over the full-V head for gamma+1 = 6 positions
+        Hv = Hd1[:6].contiguous()
+        o_v = P.HeadOutputs(1, 6, 3, V, dev)
+        for _ in range(3):
+            P.logits_topk_ids(allids, nid, W, Hv, 3, impl=args.head, out=o_v)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(reps):
+            P.logits_topk_ids(allids, nid, W, Hv, 3, impl=args.head, out=o_v)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        dense["ours_verify_top3_full_vocab_6pos_us"] = ev0.elapsed_time(ev1) * 1e3 / reps
         dense["best_dense_us"] = min(dense["cublas_topk_us"], dense["ours_full_vocab_us"])
         dense["speedup_vs_dense"] = dense["best_dense_us"] / us_head
 

@@ -17,7 +17,7 @@ timeout 600 python bench.py --config dp64 --steps 20 --warmup 3 2>&1 | tail -1 >
 cut -c1-400 gpurun_out/${T}_bench_dp64.json
 timeout 600 python bench.py --config vp32k --steps 20 --warmup 3 2>&1 | tail -1 > gpurun_out/${T}_bench_vp32k.json
 cut -c1-400 gpurun_out/${T}_bench_vp32k.json
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -s 100 -c 80 --csv --log-file gpurun_out/${T}_launches.csv python bench.py --steps 40 --warmup 5 --no-cpu --no-dense > gpurun_out/${T}_ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"head_tc" -s 30 -c 1 -o gpurun_out/${T}_fused_full python bench.py --steps 10 --warmup 5 --no-cpu --no-dense > gpurun_out/${T}_ncu_full.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"head_tc" -s 30 -c 1 -o gpurun_out/${T}_head_full python bench.py --steps 10 --warmup 5 --no-cpu --no-dense --no-fuse > gpurun_out/${T}_ncu_full2.log 2>&1
-tail -1 gpurun_out/${T}_ncu_full.log gpurun_out/${T}_ncu_full2.log
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"head_tc|state_" -s 24 -c 45 --csv --log-file gpurun_out/${T}_launches.csv python bench.py --steps 40 --warmup 5 --no-cpu --no-dense > gpurun_out/${T}_ncu_launch.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"head_tc_kernel<.int.64, .int.3>" -s 10 -c 1 -o gpurun_out/${T}_fused_full python bench.py --steps 10 --warmup 12 --no-cpu --no-dense > gpurun_out/${T}_ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"head_tc_kernel<.int.64, .int.2>" -s 30 -c 1 -o gpurun_out/${T}_head_full python bench.py --steps 10 --warmup 5 --no-cpu --no-dense --no-fuse > gpurun_out/${T}_ncu_full2.log 2>&1
+tail -n 1 gpurun_out/${T}_ncu_full.log gpurun_out/${T}_ncu_full2.log

@@ -165,3 +165,26 @@ def test_long_update_batch_longer_than_window(cuda_ok):
         st.update(0, _t(d), _t(v))
         ref.update(d, v)
         _compare(st, 0, ref)
+
+
+def test_ext_only_and_ctx_only_ablations(cuda_ok):
+    """T5 ablation sources: Ext-only = no init, the active set comes
+    from C_draft / C_ver alone (updates on a freshly created state); Ctx-only =
+    init, then no updates (the state is left as S0).  Both bit-exact vs the oracle."""
+    from paper_2605_26444_b200 import ActiveVocab
+    rng = np.random.default_rng(23)
+    V, W = 5000, 256
+    st = ActiveVocab(V, W)
+    ref = O.OracleStream(V, W)
+    for step in range(12):  # Ext-only
+        d = rng.integers(0, V, 60)
+        v = rng.integers(0, V, 3)
+        st.update(0, _t(d), _t(v))
+        ref.update(d, v)
+        _compare(st, 0, ref, what=f"ext-only step {step}")
+    st2 = ActiveVocab(V, W)  # Ctx-only
+    prompt = rng.integers(0, V, 400)
+    pre = rng.integers(0, V, (400, 3))
+    st2.init(0, _t(prompt), _t(pre))
+    ref2 = O.OracleStream(V, W).init(prompt, pre)
+    _compare(st2, 0, ref2, what="ctx-only")
