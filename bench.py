@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fuse", action="store_true", help="step = update + head as two launches")
+    ap.add_argument("--head-mode", type=int, default=-1, help="debug: force the head's reduction mode")
     ap.add_argument("--cpu-sample-steps", type=int, default=3)
     return ap.parse_args()
 
@@ -209,6 +210,9 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    if args.head_mode != -1:
+        from paper_2605_26444_b200 import _native as N
+        N.check(N.lib().nanospec_debug_set_head_mode(args.head_mode), "head mode")
     cfg = CONFIGS[args.config]
     V, d, Wm = cfg["vocab"], cfg["d"], cfg["w_max"]
     n, k = args.n_nodes, args.k

@@ -77,6 +77,7 @@ struct TcArgs {
   float* part;          // [tiles_g * S][n][128] partial tiles (split-K partials, or whole tiles for S = 1)
   uint2* cand;          // poll mode: [tiles_g][n][k + 1] level-1 lists (+ lse partial), encoded
   int mode;             // kModeCluster / kModePoll / kModeFinish / kModeFused (see the launchers)
+  int l2poll;           // cluster mode: level-1 lists self-validating, level 2 by the tile-0 CTAs polling
   // fused update + head (kModeFused): one sequence, its update and its head in one launch
   AppendArgs upd;       // the state update (fast path) of sequence upd.seq0
   unsigned* step_ctr;   // publication generation of the update's results
@@ -534,6 +535,13 @@ __device__ void level1(const TcArgs& a, int tile, int node, const int32_t* ids_s
       if (key[i]) es += __expf(v[i] - M);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
+    uint2* out = a.cand + ((long long)tile * p.n + node) * (k + 1);
+    if (a.l2poll) {  // one encoded store per entry: a poller never sees a half-written list
+      const uint2 mine = warp_topk_thr(key, gid, k, scratch);
+      if (lane < k) st_relaxed_v2(out + lane, make_uint2(mine.x ^ kEncK, mine.y ^ kEncG));
+      if (lane == 0) st_relaxed_v2(out + k, make_uint2(__float_as_uint(M) ^ kEncF, __float_as_uint(es) ^ kEncF));
+      return;
+    }
     const uint32_t T = warp_kth_key(lmk, k);
     int cnt = 0;
 #pragma unroll
@@ -543,7 +551,6 @@ __device__ void level1(const TcArgs& a, int tile, int node, const int32_t* ids_s
       if (c) scratch[cnt + __popc(bal & ((1u << lane) - 1u))] = make_uint2(key[i], gid[i]);
       cnt += __popc(bal);
     }
-    uint2* out = a.cand + ((long long)tile * p.n + node) * (k + 1);
     if (lane < k) out[lane] = make_uint2(0u, 0xffffffffu);  // padding when rows < k
     if (lane == 0) out[k] = make_uint2(__float_as_uint(M), __float_as_uint(es));
     __syncwarp();
@@ -788,6 +795,15 @@ __device__ void cluster_tail(const TcArgs& a, int tile, int split, const int32_t
   // level-2 scratch: the part of the stage area above the partial tile
   const int pbytes = (p.n * kBM * 4 + 1023) / 1024 * 1024;
   uint2* scratch = smem + pbytes / 8 + (long long)warp * ((smem_bytes - pbytes) / 8 / kWarps);
+  if (a.l2poll) {
+    // lists handed over through L2 without fences: the tile-0 CTAs poll them
+    for (int c = split + S * warp; c < p.n; c += S * kWarps) level1<false>(a, tile, c, ids_s, rows, row0, Pm, scratch);
+    if (threadIdx.x == 0) trace_mark(p.trace, 10);
+    cluster_sync();  // peers are done reading this CTA's partial tile
+    if (tin == 0)
+      for (int c = split + S * warp; c < p.n; c += S * kWarps) level2<1, true>(a, seq, c, ntiles, scratch);
+    return;
+  }
   for (int c = split + S * warp; c < p.n; c += S * kWarps) {
     level1<false>(a, tile, c, ids_s, rows, row0, Pm, scratch);
     __syncwarp();
@@ -1363,6 +1379,7 @@ cudaError_t launch_nt(const HeadProblem& p, int k, float* topk_logit, int32_t* t
   }
   a.S = S;
   a.mode = mode;
+  a.l2poll = (mode == kModeCluster && g_head_mode == 4) ? 1 : 0;
 
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(mode != kModeFinish ? tiles_g * S : (tiles_g < G ? tiles_g : G));
@@ -1474,6 +1491,7 @@ cudaError_t launch_step_nt(const HeadProblem& p, const AppendArgs& upd, int k, f
   a.tps = tiles_g;
   a.tps_reg = tps_reg;
   a.n_patch = P;
+  a.l2poll = 0;
   a.S = S;
   a.mode = kModeFused;
 

@@ -196,11 +196,12 @@ def head_mode():
     set_mode(-1)
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("mode", [0, 1, 2, 4])
 @pytest.mark.parametrize("n,k,m", [(60, 10, 3072), (1, 32, 3072), (60, 10, 129), (33, 7, 2500), (4, 10, 1)])
 def test_tc_reduction_modes(cuda_ok, llama, head_mode, mode, n, k, m):
     """Each split-K reduction / top-k hand-off of the fused tensor-core head
-    (persistent finishers, L2 hand-off, DSMEM clusters) against the oracle."""
+    (0 persistent finishers, 1 L2 hand-off, 2 DSMEM clusters, 4 DSMEM clusters
+    with the level-1 lists handed over through L2) against the oracle."""
     W, Wb = llama
     head_mode(mode)
     rng = np.random.default_rng(7 * n + m)
