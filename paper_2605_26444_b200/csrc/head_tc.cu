@@ -224,13 +224,13 @@ __device__ __forceinline__ int clamp_nact(const HeadProblem& p, int b) {
   return m < 0 ? 0 : (m > p.max_ids ? p.max_ids : m);
 }
 
-template <int NT>
+template <int NT, int UT = 1>  // UT: 128-row tiles per work unit (the persistent finisher mode takes 2)
 struct Cfg {
-  static constexpr int kABytes = kBM * kBK * 2;  // 16 KB
-  static constexpr int kBBytes = NT * kBK * 2;   // NT * 128 B
+  static constexpr int kABytes = UT * kBM * kBK * 2;  // UT x 16 KB
+  static constexpr int kBBytes = NT * kBK * 2;        // NT * 128 B
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStages = (kSmemBudget / kStageBytes) > 8 ? 8 : (kSmemBudget / kStageBytes);
-  static constexpr int kTmemCols = NT < 32 ? 32 : NT;
+  static constexpr int kTmemCols = NT * UT < 32 ? 32 : NT * UT;
   static constexpr int kStageArea = kStages * kStageBytes;
   static constexpr int kSmemBytes = kStageArea + 1024 /*align*/ + 256 /*barriers*/;
   static_assert(2 * kStages + 3 <= 30, "barrier area");
@@ -958,14 +958,17 @@ __device__ void fused_tail(const TcArgs& a, int tile, int split, const int32_t* 
 
 template <int NT, int MODE>  // one instantiation per mode: only its own tail is compiled in
 __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
-  using C = Cfg<NT>;
+  // the persistent finisher mode processes two row tiles per unit: two MMAs per
+  // K step share the hidden-state operand, so H crosses L2 half as often
+  constexpr int UT = MODE == kModeFinish ? 2 : 1;
+  using C = Cfg<NT, UT>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B aligned view that keeps the shared address space visible to the compiler
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStageArea);
   // bars[0..S) full, [S..2S) empty, [2S] tmem_full, [2S+1] tmem_empty
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::kStages + 2);
-  __shared__ int32_t ids_s[kBM];   // the unit's row ids
+  __shared__ int32_t ids_s[kBM * UT];   // the unit's row ids
   __shared__ int sh_m;
 
   const HeadProblem& p = a.p;
@@ -1039,8 +1042,12 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
     }
     return;
   }
-  for (int tile = first; tile < tiles_g; tile += step) {
-    const int seq = tile / a.tps, tin = tile - (tile / a.tps) * a.tps;
+  const int tpu = (a.tps + UT - 1) / UT;  // units per sequence
+  const int units_g = UT == 1 ? tiles_g : p.batch * tpu;
+  for (int unit = first; unit < units_g; unit += step) {
+    const int seq = unit / tpu, t0 = (unit - seq * tpu) * UT;  // first tile of the unit within its sequence
+    const int tile = seq * a.tps + t0;
+    const int tin = t0;
     int row0 = tin * kBM;
     int m;
     if (MODE == kModeFused && tile >= a.tps_reg) {
@@ -1060,15 +1067,16 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
     } else {
       // one round trip: the tile's ids (rows past n_active are never dereferenced)
       // and n_active
-      if (tid < kBM) ids_s[tid] = row0 + tid < p.max_ids ? __ldcg(p.ids_base + (long long)seq * p.ids_stride + row0 + tid) : 0;
-      if (tid == kBM) sh_m = clamp_nact(p, seq);
+      if (tid < kBM * UT)
+        ids_s[tid] = row0 + tid < p.max_ids ? __ldcg(p.ids_base + (long long)seq * p.ids_stride + row0 + tid) : 0;
+      if (tid == kBM * UT) sh_m = clamp_nact(p, seq);
       if (MODE == kModeFused && tid == kBM + 1) sh_g0 = ld_acquire(a.step_ctr);  // same round trip
       __syncthreads();
       if (MODE == kModeFused && tid == 0) red_add_release(a.arrive_ctr, 1u);  // pre-update ids / n_active read
       m = sh_m;
     }
     if (tid == 0 && local == 0) trace_mark(p.trace, 7);  // ids + n_active in shared memory
-    const int rows = min(kBM, m - row0);
+    const int rows = min(kBM * UT, m - row0);  // rows of the unit (UT tiles)
     if (rows <= 0) {  // past n_active: every CTA of the tile skips it
       __syncthreads();
       if (MODE == kModeFused && patch_rows) local = -1;  // fused: the empty patch tile still publishes padding
@@ -1084,12 +1092,13 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
 
     if (warp < kLoadWarps) {
       // ---------------- producers: gather rows of W_head + H into SW128 stages
-      const uint16_t* rp[2];
+      const uint16_t* rp[2 * UT];  // rows lr + 64 i (i < 2) of each of the UT tiles
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int32_t g = ids_s[lr + 64 * i];
+      for (int i = 0; i < 2 * UT; ++i) {
+        const int ur = (i >> 1) * kBM + lr + 64 * (i & 1);
+        const int32_t g = ids_s[ur];
         const long long row = p.n_shards > 1 ? g / p.n_shards : g;
-        rp[i] = (lr + 64 * i < rows) ? p.w + row * p.ldw + (tid & 7) * 8 : nullptr;
+        rp[i] = (ur < rows) ? p.w + row * p.ldw + (tid & 7) * 8 : nullptr;
       }
       const uint16_t* hp = p.h + (long long)seq * p.n * p.d + (tid & 7) * 8;
       if (tid == 0 && local == 0) trace_mark(p.trace, 2);  // row pointers ready, first loads next
@@ -1102,9 +1111,9 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
           const uint32_t sB = sA + C::kABytes;
           const int kcol = (kb0 + q) * kBK;
 #pragma unroll
-          for (int i = 0; i < 2; ++i)
-            cp_async16(sA + (lr + 64 * i) * 128 + swz, rp[i] ? (const void*)(rp[i] + kcol) : (const void*)p.w,
-                       rp[i] ? 16u : 0u);
+          for (int i = 0; i < 2 * UT; ++i)
+            cp_async16(sA + (i >> 1) * (kBM * 128) + (lr + 64 * (i & 1)) * 128 + swz,
+                       rp[i] ? (const void*)(rp[i] + kcol) : (const void*)p.w, rp[i] ? 16u : 0u);
 #pragma unroll
           for (int i = 0; i < (C::kHChunks + kLoaders - 1) / kLoaders; ++i) {
             const int hr = lr + 64 * i;
@@ -1133,13 +1142,16 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
       const int r = lg * 32 + lane;               // TMEM lane == tile row
       const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16);
       // per column, the 32 lanes of a warp store 128 consecutive bytes
+#pragma unroll 1
+      for (int h = 0; h < UT; ++h) {
+      if (h > 0 && (t0 + h >= a.tps || row0 + h * kBM >= m)) break;  // the unit's second tile is empty
       float* Pw = (MODE == kModeCluster || MODE == kModeFused) ? reinterpret_cast<float*>(smem) + r
-                                         : a.part + (((long long)tile * S + split) * p.n) * kBM + r;
+                                         : a.part + (((long long)(tile + h) * S + split) * p.n) * kBM + r;
       if (cgp < C::kColGroups) {
 #pragma unroll 1
         for (int c0 = cgp * 16; c0 < NT && c0 < p.n; c0 += 16 * C::kColGroups) {
           float v[16];
-          tmem_ld16(taddr + c0, v);
+          tmem_ld16(taddr + h * NT + c0, v);
 #pragma unroll
           for (int c = 0; c < 16; ++c)
             if (c0 + c < p.n) {
@@ -1150,6 +1162,7 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
             }
         }
       }
+      }  // tiles of the unit
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&bars[2 * C::kStages + 1]));
@@ -1174,7 +1187,10 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
           const uint32_t sB = sA + C::kABytes;
 #pragma unroll
           for (int kk = 0; kk < kBK / 16; ++kk)
-            umma_bf16(tmem, sw128_desc(sA + kk * 32), sw128_desc(sB + kk * 32), idesc, (q | kk) ? 1u : 0u);
+#pragma unroll
+            for (int h = 0; h < UT; ++h)  // tile h of the unit into TMEM columns [h NT, (h + 1) NT)
+              umma_bf16(tmem + h * NT, sw128_desc(sA + h * (kBM * 128) + kk * 32), sw128_desc(sB + kk * 32), idesc,
+                        (q | kk) ? 1u : 0u);
           umma_commit(smem_u32(&bars[C::kStages + stage]));
           if (q == nk - 1) umma_commit(smem_u32(&bars[2 * C::kStages]));
         }
@@ -1302,8 +1318,8 @@ cudaError_t launch_nt(const HeadProblem& p, int k, float* topk_logit, int32_t* t
   using C = Cfg<NT>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e =
-        cudaFuncSetAttribute(head_tc_kernel<NT, kModeFinish>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    cudaError_t e = cudaFuncSetAttribute(head_tc_kernel<NT, kModeFinish>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg<NT, 2>::kSmemBytes);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(head_tc_kernel<NT, kModePoll>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e == cudaSuccess)
@@ -1382,9 +1398,10 @@ cudaError_t launch_nt(const HeadProblem& p, int k, float* topk_logit, int32_t* t
   a.l2poll = (mode == kModeCluster && g_head_mode == 4) ? 1 : 0;
 
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(mode != kModeFinish ? tiles_g * S : (tiles_g < G ? tiles_g : G));
+  const int units2 = p.batch * ((a.tps + 1) / 2);  // finisher mode: two tiles per unit
+  cfg.gridDim = dim3(mode != kModeFinish ? tiles_g * S : (units2 < G ? units2 : G));
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = C::kSmemBytes;
+  cfg.dynamicSmemBytes = mode == kModeFinish ? Cfg<NT, 2>::kSmemBytes : C::kSmemBytes;
   cfg.stream = stream;
   cudaLaunchAttribute attrs[2];
   int na = 0;
