@@ -64,6 +64,7 @@ constexpr uint32_t kEncF = 0x7fbadbadu;  // partial logits / lse floats: a NaN p
 constexpr uint32_t kEncK = 0x00000001u;  // list keys: float_key(v) == 1 only for NaN bit patterns
 constexpr uint32_t kEncG = 0x7fffffffu;  // list ids: valid ids are < 2^31 - 1, padding is 0xffffffff
 constexpr int kModeFinish = 0;   // persistent CTAs, grid barrier, one finisher CTA per (sequence, node)
+constexpr int kModeFinishWide = 5;  // the same with two row tiles per unit (capacity >= 2 x #SMs tiles)
 constexpr int kModePoll = 1;     // one unit per CTA, split-K partials + lists handed over through L2
 constexpr int kModeCluster = 2;  // one unit per CTA, the S splits of a tile form a cluster (DSMEM reduction)
 constexpr int kModeFused = 3;    // cluster mode + the state update in the same launch (patch tiles)
@@ -960,7 +961,7 @@ template <int NT, int MODE>  // one instantiation per mode: only its own tail is
 __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
   // the persistent finisher mode processes two row tiles per unit: two MMAs per
   // K step share the hidden-state operand, so H crosses L2 half as often
-  constexpr int UT = MODE == kModeFinish ? 2 : 1;
+  constexpr int UT = MODE == kModeFinishWide ? 2 : 1;
   using C = Cfg<NT, UT>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B aligned view that keeps the shared address space visible to the compiler
@@ -1318,8 +1319,11 @@ cudaError_t launch_nt(const HeadProblem& p, int k, float* topk_logit, int32_t* t
   using C = Cfg<NT>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(head_tc_kernel<NT, kModeFinish>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg<NT, 2>::kSmemBytes);
+    cudaError_t e =
+        cudaFuncSetAttribute(head_tc_kernel<NT, kModeFinish>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(head_tc_kernel<NT, kModeFinishWide>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               Cfg<NT, 2>::kSmemBytes);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(head_tc_kernel<NT, kModePoll>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     if (e == cudaSuccess)
@@ -1398,10 +1402,14 @@ cudaError_t launch_nt(const HeadProblem& p, int k, float* topk_logit, int32_t* t
   a.l2poll = (mode == kModeCluster && g_head_mode == 4) ? 1 : 0;
 
   cudaLaunchConfig_t cfg = {};
-  const int units2 = p.batch * ((a.tps + 1) / 2);  // finisher mode: two tiles per unit
-  cfg.gridDim = dim3(mode != kModeFinish ? tiles_g * S : (units2 < G ? units2 : G));
+  // finisher mode: two tiles per unit once the tile capacity is at least twice
+  // the SM count (halves the hidden-state traffic without starving SMs; the
+  // host cannot see n_active, so the rule is on capacity)
+  const bool wide = mode == kModeFinish && tiles_g >= 2 * G;
+  const int units2 = p.batch * ((a.tps + 1) / 2);
+  cfg.gridDim = dim3(mode != kModeFinish ? tiles_g * S : wide ? (units2 < G ? units2 : G) : (tiles_g < G ? tiles_g : G));
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = mode == kModeFinish ? Cfg<NT, 2>::kSmemBytes : C::kSmemBytes;
+  cfg.dynamicSmemBytes = wide ? Cfg<NT, 2>::kSmemBytes : C::kSmemBytes;
   cfg.stream = stream;
   cudaLaunchAttribute attrs[2];
   int na = 0;
@@ -1419,7 +1427,8 @@ cudaError_t launch_nt(const HeadProblem& p, int k, float* topk_logit, int32_t* t
   cfg.numAttrs = na;
   auto kern = mode == kModeCluster ? head_tc_kernel<NT, kModeCluster>
               : mode == kModePoll  ? head_tc_kernel<NT, kModePoll>
-                                   : head_tc_kernel<NT, kModeFinish>;
+                     : wide              ? head_tc_kernel<NT, kModeFinishWide>
+                                         : head_tc_kernel<NT, kModeFinish>;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
   if (e != cudaSuccess) {
     (void)cudaGetLastError();

@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(kThreads, 1) gather_kernel(Args a, const __gri
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (sa(smem_raw) & 1023u)) & 1023u);
   __shared__ __align__(8) uint64_t bars[16];
-  __shared__ int rid[128];
+  __shared__ int rid[256];
   const int tid = threadIdx.x;
   float acc = 0.f;
   if (tid == 0) {
@@ -62,6 +62,37 @@ __global__ void __launch_bounds__(kThreads, 1) gather_kernel(Args a, const __gri
     a.t[512 + blockIdx.x] = t0;
   }
   if (MODE == 9) {
+  } else if (MODE == 10 || MODE == 11) {
+    // the head's stage pattern: UT tiles of 128 rows x a K chunk, plus 60 hidden-state
+    // rows (64-row stage, 4 zero-filled) from a small L2-resident H, 8-stage budget of 192 KB
+    constexpr int UT = MODE == 11 ? 2 : 1;
+    constexpr int kStage = UT * 16384 + 8192;
+    constexpr int kSt = (196608 / kStage) > 8 ? 8 : 196608 / kStage;
+    const int unit = blockIdx.x / a.S, split = blockIdx.x % a.S;
+    const int KB = D / 64, kb0 = split * KB / a.S, kb1 = (split + 1) * KB / a.S, nk = kb1 - kb0;
+    if (tid < 128 * UT) rid[tid] = a.ids[unit * 128 * UT + tid];
+    __syncthreads();
+    const int lr = tid >> 3;
+    const int swz = ((tid & 7) ^ (lr & 7)) << 4;
+    const uint16_t* hbase = a.w + (long long)(V - 64) * D;  // H: 60 rows near the end of W (L2-resident after the first CTAs)
+    for (int q = 0; q < nk; ++q) {
+      const uint32_t st = sa(sm + (q % kSt) * kStage);
+      const int col = (kb0 + q) * 64;
+#pragma unroll
+      for (int i = 0; i < 2 * UT; ++i) {
+        const int ur = (i >> 1) * 128 + lr + 64 * (i & 1);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(st + (i >> 1) * 16384 + (lr + 64 * (i & 1)) * 128 + swz),
+                     "l"(a.w + (long long)rid[ur] * D + (tid & 7) * 8 + col) : "memory");
+      }
+      if (lr < 64)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(st + UT * 16384 + lr * 128 + swz),
+                     "l"(hbase + (long long)lr * D + (tid & 7) * 8 + col), "r"(lr < 60 ? 16 : 0) : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group %0;" ::"n"(kSt - 1) : "memory");
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    acc = reinterpret_cast<float*>(sm)[tid];
   } else if (MODE == 8) {
     // K-split, M0's lane mapping (8 threads per 128-B row piece), every stage in flight at once
     const int tile = blockIdx.x / a.S, split = blockIdx.x % a.S;
@@ -329,6 +360,10 @@ int main() {
       run("M1 tma gather4 k-split ring", gather_kernel<1>, 24 * S, 8 * 16384 + 1024, S, cold);
     }
     run("M8 cp.async k-split ALL in flight", gather_kernel<8>, 120, 13 * 16384 + 1024, 5, cold);
+    run("M10 head pattern +H, 24x5", gather_kernel<10>, 120, 196608 + 1024, 5, cold);
+    run("M10 head pattern +H, 24x6", gather_kernel<10>, 144, 196608 + 1024, 6, cold);
+    run("M11 head pattern +H, 2 tiles/CTA, 12x8", gather_kernel<11>, 96, 196608 + 1024, 8, cold);
+    run("M11 head pattern +H, 2 tiles/CTA, 12x12", gather_kernel<11>, 144, 196608 + 1024, 12, cold);
     run("M6 cp.async k-split ring4x32K", gather_kernel<6>, 120, 4 * 32768 + 1024, 5, cold);
     run("M7 cp.async k-split all-in-flight", gather_kernel<7>, 120, 7 * 32768 + 1024, 5, cold);
     run("M2 tma gather4 row-split", gather_kernel<2>, 148, 64 * 24 * 128 + 1024, 1, cold);
