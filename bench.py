@@ -359,55 +359,29 @@ def run_ours(args):
     extra["us_draft_round_1x1_5x10"] = timed(draft_round, max(R, K // 6))
     extra = {kk: round(vv, 3) for kk, vv in extra.items()}
 
-    # e2e through the public API with host buffers, every step: ONE H2D copy of
-    # the step's inputs (hidden states + draft ids + verify ids, packed in one
-    # pinned block) and ONE D2H copy of its results (top-k values, ids, lse,
-    # packed), around the step call
-    hb, lb_ = n * d * 2, 63 * 4
-    in_bytes = hb + lb_
+    # e2e through the C ABI with HOST buffers (nanospec_step_host): every step one
+    # H2D copy of the packed inputs (hidden states + draft ids + verify ids, a
+    # pinned block prepared beforehand), the step, one D2H copy of the packed
+    # results (top-k values, ids, lse)
     E = K
+    io = P.StepHostIO(n, d, 60, 3, k, Wm, dev)
     blocks = []
-    for s_ in range(E):  # the inputs of step s_, staged host-side beforehand (pinned)
+    for s_ in range(E):
         r = s_ % R
         c = cursor[r] + s_ // R
-        blk = torch.empty(in_bytes, dtype=torch.uint8).pin_memory()
-        blk[:hb].view(torch.bfloat16).copy_(Hs[r].reshape(-1).cpu())
-        blk[hb:hb + 240].view(torch.int32).copy_(upd_d[r][c].cpu())
-        blk[hb + 240:].view(torch.int32).copy_(upd_v[r][c].cpu())
-        blocks.append(blk)
-    din = torch.empty(in_bytes, dtype=torch.uint8, device=dev)
-    Hd = din[:hb].view(torch.bfloat16).view(n, d)
-    ud_d = din[hb:hb + 240].view(torch.int32)
-    uv_d = din[hb + 240:].view(torch.int32)
-    ob = n * k * 4
-    e2e_out = []
-    for r in range(R):  # results of sequence r packed in one device buffer: [logit | id | lse]
-        buf = torch.empty(2 * ob + n * 4, dtype=torch.uint8, device=dev)
-        o = P.HeadOutputs(1, n, k, Wm, dev)
-        o.topk_logit = buf[:ob].view(torch.float32).view(1, n, k)
-        o.topk_id = buf[ob:2 * ob].view(torch.int32).view(1, n, k)
-        o.lse = buf[2 * ob:].view(torch.float32).view(1, n)
-        e2e_out.append((buf, o))
-    hout = torch.empty(2 * ob + n * 4, dtype=torch.uint8).pin_memory()
+        blocks.append((r, io.pack_inputs(Hs[r], upd_d[r][c], upd_v[r][c])))
     torch.cuda.synchronize()
     ev0.record(stream)
     for s_ in range(E):
-        r = s_ % R
+        r, blk = blocks[s_]
         cursor[r] += 1
-        din.copy_(blocks[s_], non_blocking=True)
-        buf, o = e2e_out[r]
-        if fused:
-            P.step(states[r], 0, ud_d, uv_d, W, Hd, k, out=o)
-        else:
-            states[r].update(0, ud_d, uv_d)
-            P.draft_logits_topk(states[r], W, Hd.view(1, n, d), k, impl=args.head, out=o)
-        hout.copy_(buf, non_blocking=True)
+        P.step_host(states[r], 0, io, blk, W, k)
     ev1.record(stream)
     torch.cuda.synchronize()
     us_e2e = ev0.elapsed_time(ev1) * 1e3 / E
     assert all(st.read(0)["n_active"] == Wm for st in states)
-    h2d = in_bytes
-    d2h = 2 * ob + n * 4
+    h2d = n * d * 2 + 63 * 4
+    d2h = n * k * 8 + n * 4
 
     # dense comparators: cuBLAS bf16 GEMM (fp32 accumulate) + torch.topk, and our head over [0, V)
     dense = {}

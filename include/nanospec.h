@@ -230,6 +230,20 @@ nanospec_status nanospec_step(nanospec_state st, int32_t seq, const int32_t* d_d
                               int32_t* d_topk_id, float* d_lse, void* d_scratch, size_t scratch_bytes,
                               cudaStream_t stream);
 
+/* nanospec_step with HOST buffers (the end-to-end call): one host->device copy
+ * of the packed inputs, the step, one device->host copy of the packed results,
+ * all asynchronous on `stream` (pinned host memory for real overlap).
+ *   h_in  = [hidden bf16 n_nodes x d_model][draft int32 n_draft][verify int32 k_ver]
+ *   h_out = [topk_logit fp32 n_nodes x k][topk_id int32 n_nodes x k][lse fp32 n_nodes]
+ *   d_io  : caller-owned device staging, >= nanospec_step_host_io_bytes(...)
+ *   d_scratch as for nanospec_step.  h_out is valid after the stream syncs. */
+size_t nanospec_step_host_io_bytes(int32_t n_nodes, int32_t d_model, int32_t n_draft, int32_t k_ver, int32_t k,
+                                   size_t* in_bytes, size_t* out_bytes);
+nanospec_status nanospec_step_host(nanospec_state st, int32_t seq, const void* h_in, int32_t n_draft, int32_t k_ver,
+                                   const void* d_w_head, int32_t d_model, int64_t ldw, int32_t n_nodes, int32_t k,
+                                   void* h_out, void* d_io, size_t io_bytes, void* d_scratch, size_t scratch_bytes,
+                                   cudaStream_t stream);
+
 /* 1 if nanospec_step with these sizes runs as ONE fused launch on the current
  * device, 0 if it runs as update + head (same results).  Host-only query. */
 int32_t nanospec_step_fused(const nanospec_state st, int32_t n_draft, int32_t k_ver, int32_t d_model,

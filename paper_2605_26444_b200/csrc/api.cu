@@ -339,6 +339,41 @@ nanospec_status nanospec_step(nanospec_state st, int32_t seq, const int32_t* d_d
                   stream);
 }
 
+size_t nanospec_step_host_io_bytes(int32_t n_nodes, int32_t d_model, int32_t n_draft, int32_t k_ver, int32_t k,
+                                   size_t* in_bytes, size_t* out_bytes) {
+  if (n_nodes < 1 || d_model <= 0 || n_draft < 0 || k_ver < 0 || k < 1) return 0;
+  const size_t ib = align_up((size_t)n_nodes * d_model * 2 + (size_t)(n_draft + k_ver) * 4);
+  const size_t ob = align_up((size_t)n_nodes * k * 8 + (size_t)n_nodes * 4);
+  if (in_bytes) *in_bytes = ib;
+  if (out_bytes) *out_bytes = ob;
+  return ib + ob;
+}
+
+nanospec_status nanospec_step_host(nanospec_state st, int32_t seq, const void* h_in, int32_t n_draft, int32_t k_ver,
+                                   const void* d_w_head, int32_t d_model, int64_t ldw, int32_t n_nodes, int32_t k,
+                                   void* h_out, void* d_io, size_t io_bytes, void* d_scratch, size_t scratch_bytes,
+                                   cudaStream_t stream) {
+  if (!h_in || !h_out || !d_io) return NANOSPEC_EINVAL;
+  size_t ib = 0, ob = 0;
+  if (nanospec_step_host_io_bytes(n_nodes, d_model, n_draft, k_ver, k, &ib, &ob) == 0 || io_bytes < ib + ob)
+    return NANOSPEC_EINVAL;
+  char* din = (char*)d_io;
+  char* dout = din + ib;
+  const size_t hb = (size_t)n_nodes * d_model * 2;
+  const size_t in_used = hb + (size_t)(n_draft + k_ver) * 4;
+  const size_t out_used = (size_t)n_nodes * k * 8 + (size_t)n_nodes * 4;
+  if (cudaMemcpyAsync(din, h_in, in_used, cudaMemcpyHostToDevice, stream) != cudaSuccess) return NANOSPEC_ECUDA;
+  const int32_t* dd = n_draft > 0 ? (const int32_t*)(din + hb) : nullptr;
+  const int32_t* dv = k_ver > 0 ? (const int32_t*)(din + hb) + n_draft : nullptr;
+  float* ol = (float*)dout;
+  int32_t* oi = (int32_t*)(dout + (size_t)n_nodes * k * 4);
+  float* os = (float*)(dout + (size_t)n_nodes * k * 8);
+  nanospec_status r = nanospec_step(st, seq, dd, n_draft, dv, k_ver, d_w_head, d_model, ldw, din, n_nodes, k, ol, oi,
+                                    os, d_scratch, scratch_bytes, stream);
+  if (r != NANOSPEC_OK) return r;
+  return cuda_status(cudaMemcpyAsync(h_out, dout, out_used, cudaMemcpyDeviceToHost, stream));
+}
+
 int32_t nanospec_step_fused(const nanospec_state st, int32_t n_draft, int32_t k_ver, int32_t d_model,
                             int32_t n_nodes, int32_t k) {
   if (!st || n_draft < 0 || k_ver < 0 || d_model <= 0 || d_model % 8 != 0) return 0;

@@ -208,6 +208,53 @@ def step(state: ActiveVocab, seq: int, draft: torch.Tensor | None, verify: torch
     return out.topk_logit, out.topk_id, out.lse
 
 
+class StepHostIO:
+    """Device staging for nanospec_step_host (the end-to-end call with HOST
+    buffers): pinned host blocks in the ABI's packed layouts
+    in  = [hidden bf16 n x d][draft int32 n_draft][verify int32 k_ver],
+    out = [topk_logit fp32 n x k][topk_id int32 n x k][lse fp32 n]."""
+
+    def __init__(self, n_nodes: int, d_model: int, n_draft: int, k_ver: int, k: int, w_max: int, device):
+        ib, ob = ctypes.c_size_t(0), ctypes.c_size_t(0)
+        total = N.lib().nanospec_step_host_io_bytes(n_nodes, d_model, n_draft, k_ver, k, ctypes.byref(ib),
+                                                    ctypes.byref(ob))
+        if total == 0:
+            raise N.NanoSpecError(N.EINVAL, "nanospec_step_host_io_bytes")
+        self.n, self.d, self.n_draft, self.k_ver, self.k = n_nodes, d_model, n_draft, k_ver, k
+        self.in_bytes, self.out_bytes = ib.value, ob.value
+        self.d_io = torch.empty(total, dtype=torch.uint8, device=device)
+        self.scratch = HeadOutputs(1, n_nodes, k, w_max, device).scratch
+        self.h_out = torch.empty(self.out_bytes, dtype=torch.uint8).pin_memory()
+
+    def pack_inputs(self, hidden: torch.Tensor, draft, verify) -> torch.Tensor:
+        """A pinned host block holding one step's inputs."""
+        blk = torch.zeros(self.in_bytes, dtype=torch.uint8).pin_memory()
+        hb = self.n * self.d * 2
+        blk[:hb].view(torch.bfloat16).copy_(hidden.reshape(-1).cpu())
+        blk[hb:hb + 4 * self.n_draft].view(torch.int32).copy_(torch.as_tensor(draft, dtype=torch.int32).cpu())
+        blk[hb + 4 * self.n_draft:hb + 4 * (self.n_draft + self.k_ver)].view(torch.int32).copy_(
+            torch.as_tensor(verify, dtype=torch.int32).cpu())
+        return blk
+
+    def results(self):
+        """(topk_logit [n,k], topk_id [n,k], lse [n]) views of the host result block."""
+        nk = self.n * self.k
+        return (self.h_out[:4 * nk].view(torch.float32).view(self.n, self.k),
+                self.h_out[4 * nk:8 * nk].view(torch.int32).view(self.n, self.k),
+                self.h_out[8 * nk:8 * nk + 4 * self.n].view(torch.float32))
+
+
+def step_host(state: ActiveVocab, seq: int, io: StepHostIO, h_in: torch.Tensor, w_head: torch.Tensor, k: int):
+    """nanospec_step_host: H2D of the packed inputs, the step, D2H of the packed
+    results, asynchronous on the current stream (results in io.results() after a sync)."""
+    _need(w_head, torch.bfloat16, "w_head")
+    st = N.lib().nanospec_step_host(
+        state.handle, seq, h_in.data_ptr(), io.n_draft, io.k_ver, _ptr(w_head), io.d, w_head.stride(0), io.n, k,
+        io.h_out.data_ptr(), _ptr(io.d_io), io.d_io.numel(), _ptr(io.scratch), io.scratch.numel(),
+        _stream(w_head.device))
+    N.check(st, "nanospec_step_host")
+
+
 def step_is_fused(state: ActiveVocab, n_draft: int, k_ver: int, d_model: int, n_nodes: int, k: int) -> bool:
     """Whether step() with these sizes runs as one fused launch on this device."""
     return bool(N.lib().nanospec_step_fused(state.handle, n_draft, k_ver, d_model, n_nodes, k))

@@ -198,3 +198,26 @@ def test_step_many_back_to_back(cuda_ok, llama):
         ids = _check_state(sts[r], refs[r], f"seq {r}")
         v, i, l = outs[r].topk_logit, outs[r].topk_id, outs[r].lse
         _check_head(v, i, l, ids, Wb, Hs[r], k, f"graph seq {r}")
+
+
+def test_step_host_buffers(cuda_ok, llama):
+    """nanospec_step_host: packed host inputs -> step -> packed host results
+    equals the oracle (the end-to-end call the bench times)."""
+    from paper_2605_26444_b200 import ActiveVocab, StepHostIO, step_host
+    W, Wb = llama
+    V, d = W.shape
+    Wm, n, k = 3072, 60, 10
+    pool = SI.disjoint_pools(V, Wm + 126, 1, seed=21)[0]
+    prompt, ups = SI.cyclic_fresh_updates(pool, Wm, 3)
+    st = ActiveVocab(V, Wm)
+    st.init(0, _t(prompt))
+    ref = O.OracleStream(V, Wm).init(prompt)
+    io = StepHostIO(n, d, 60, 3, k, Wm, "cuda")
+    for s, (dd, vv) in enumerate(ups):
+        H = SI.bf16_hidden(n, d, seed=500 + s, device="cuda")
+        step_host(st, 0, io, io.pack_inputs(H, dd, vv), W, k)
+        torch.cuda.synchronize()
+        ref.update(dd, vv)
+        ids = _check_state(st, ref, f"host step {s}")
+        v, i, l = io.results()
+        _check_head(v.unsqueeze(0), i.unsqueeze(0), l.unsqueeze(0), ids, Wb, H, k, f"host step {s}")
