@@ -12,24 +12,31 @@
 //
 // Contraction.  UMMA M = 128 active rows (A), N = NT >= n nodes (B, zero
 // padded), K = 64 per pipeline stage; D in TMEM (NT fp32 columns).  A launch
-// covers tiles_g = batch * ceil(max_ids / 128) row tiles (tiles past a
-// sequence's n_active, read from device memory, exit at once).  With
-// tiles_g < #SMs every tile is split along K into S = #SMs / tiles_g chunks
-// (S = 6 at |I| = 3072: 144 CTAs stream), one CTA per (tile, chunk); with
-// tiles_g >= #SMs (e.g. the dense [0, V) comparator) S = 1 and persistent CTAs
-// loop over tiles.
+// covers batch * ceil(max_ids / 128) row tiles (tiles past a sequence's
+// n_active, read from device memory, are skipped).  Fewer tiles than SMs: every
+// tile is split along K over S CTAs; more: persistent CTAs loop over tiles.
 //
-// Reduction + top-k: every CTA drains its partial tile from TMEM straight to
-// an L2-resident buffer P[tile][split][node][128] and arrives at a one-word
-// grid counter (arrivals in the low bits; the last arriver bumps a generation
-// field).  CTAs 0 .. batch*n-1 are the finishers of the (sequence, node) pairs:
-// they wait for the generation to change, sum the S partials of every active
-// row in split order (fixed order: equal rows give bit-equal logits), keep the
-// online (max, sum exp) for lse, and select the top-k in registers (per-thread
-// sorting network, then k rounds of a warp arg-max by two redux instructions,
-// then a merge of the per-warp lists).  The other CTAs leave as soon as they
-// have arrived.  All CTAs of a launch are co-resident (grid <= #SMs, one CTA
-// per SM), so the finishers' wait cannot deadlock.
+// Split-K reduction + top-k, one of four modes (chosen by the launchers):
+//  * cluster (the headline): the S CTAs of a tile form a thread-block cluster
+//    (S = largest <= 8 with every cluster co-resident: 5 at |I| = 3072); each
+//    drains its partial tile TMEM -> smem, and after a cluster barrier CTA s
+//    sums the nodes s, s+S, ... over DSMEM in K-chunk order (deterministic),
+//    one warp per (tile, node) takes the exact level-1 top-k (threshold = k-th
+//    largest lane maximum, compaction, rank by counting) + (max, sum exp); a
+//    per-node arrival counter (release/acquire) lets the last tile's warp
+//    merge the node's lists (level 2, one round trip) -- nobody waits;
+//  * poll (> 32 tiles per sequence, one unit per CTA): partials and lists go
+//    through L2 as self-validating words (stored XOR a constant no value
+//    equals; the consumer re-zeroes), no fences or flags;
+//  * finisher (persistent): whole-tile partials to L2 (two tiles per unit when
+//    the capacity is >= 2x the SMs, sharing H), a one-word grid barrier, then
+//    one finisher CTA per (sequence, node) sums, keeps an online lse and
+//    selects the top-k (sorting network + warp arg-max rounds);
+//  * fused step (nanospec_step): cluster mode over the pre-update slots plus
+//    patch tiles for the update-list ids, with one extra cluster whose CTA 0
+//    runs the state update (state_fast.cuh) while everything streams.
+// Every mode relies on all CTAs of a launch being co-resident (grid <= #SMs,
+// one CTA per SM, cluster counts from cudaOccupancyMaxActiveClusters).
 //
 // Warp roles (544 threads): warps 0-15 load (cp.async) and drain TMEM (warp w
 // reads TMEM lanes 32*(w%4).. and a quarter of the columns); warp 16 allocates
