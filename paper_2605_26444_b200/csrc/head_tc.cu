@@ -489,15 +489,13 @@ __device__ void level1(const TcArgs& a, int tile, int node, const int32_t* ids_s
   float v[4] = {0.f, 0.f, 0.f, 0.f};
   if (!kPollMode) {
     const uint32_t la = smem_u32(Pm + node * kBM + 4 * lane);
-    for (int j0 = 0; j0 < S; j0 += 4) {
-      float4 x[4];
+    float4 x[kMaxCluster];  // all S partials in flight at once (one DSMEM round trip)
 #pragma unroll
-      for (int j = 0; j < 4; ++j)  // K chunk j of this tile was computed by cluster rank (j - tile) mod S
-        if (j0 + j < S) x[j] = ld_dsmem_v4(mapa_shared(la, (uint32_t)((j0 + j + S - tile % S) % S)));
+    for (int j = 0; j < kMaxCluster; ++j)  // K chunk j of this tile was computed by cluster rank (j - tile) mod S
+      if (j < S) x[j] = ld_dsmem_v4(mapa_shared(la, (uint32_t)((j + S - tile % S) % S)));
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (j0 + j < S) { v[0] += x[j].x; v[1] += x[j].y; v[2] += x[j].z; v[3] += x[j].w; }  // K-chunk order
-    }
+    for (int j = 0; j < kMaxCluster; ++j)
+      if (j < S) { v[0] += x[j].x; v[1] += x[j].y; v[2] += x[j].z; v[3] += x[j].w; }  // K-chunk order
   }
   for (int s0 = 0; kPollMode && s0 < S; s0 += 8) {
     uint4 x[8];
