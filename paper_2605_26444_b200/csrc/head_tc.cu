@@ -224,6 +224,11 @@ __device__ __forceinline__ float4 ld_dsmem_v4(uint32_t caddr) {
   return v;
 }
 __device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v);
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void red_add_release(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -902,15 +907,6 @@ __device__ int fused_unique_ids(const TcArgs& a, int32_t* sm, int base, int32_t*
   return nu;
 }
 
-__device__ __forceinline__ bool hash_contains(const int32_t* keys, int32_t key) {
-  int h = hash_slot(key);
-  while (true) {
-    const int32_t k2 = keys[h];
-    if (k2 == key) return true;
-    if (k2 == -1) return false;
-    h = (h + 1) & (kHashSlots - 1);
-  }
-}
 
 // Tail of a fused-step CTA (cluster mode), after the update has published:
 // regular tiles drop the rows whose id left I (stale slots), patch tiles keep
@@ -928,21 +924,11 @@ __device__ void fused_tail(const TcArgs& a, int tile, int split, const int32_t* 
   const int ntiles = nreg + a.n_patch;
   const int row0 = patch ? (tile - a.tps_reg) * kBM : tile * kBM;
   const int rows = min(kBM, (patch ? nu : m_old) - row0);
-  const int hash_bytes = kHashSlots * 4;
-  int32_t* hkey = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(smem) + smem_bytes - hash_bytes);
-  uint32_t drop4 = 0u;  // this lane's rows (4 * lane + i) that do not count
-  if (!patch) {
-    drop4 = (stale_tile[lane >> 3] >> ((lane & 7) * 4)) & 0xfu;  // fetched by the MMA warp
-  } else {
-    const int ne = __ldcg(&a.enter_meta[0]);
-    for (int h = threadIdx.x; h < kHashSlots; h += blockDim.x) hkey[h] = -1;
-    __syncthreads();
-    for (int t = threadIdx.x; t < ne; t += blockDim.x) hash_insert(hkey, __ldcg(&a.enter_ids[t]));
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (4 * lane + i < rows && !hash_contains(hkey, ids_s[4 * lane + i])) drop4 |= 1u << i;
-  }
+  const int hash_bytes = kHashSlots * 4;  // reserved at the end of the stage area (launcher accounting)
+  // this lane's rows (4 * lane + i) that do not count: stale slots (regular
+  // tiles) or ids already active before the update (patch tiles); the mask
+  // was built by loader warp 15 during the stream (empty patch tiles: none)
+  const uint32_t drop4 = rows > 0 ? (stale_tile[lane >> 3] >> ((lane & 7) * 4)) & 0xfu : 0u;
   cluster_sync();  // every CTA of the cluster has its partial tile in shared memory
   if (threadIdx.x == 0) trace_mark(p.trace, 5);
   const int pbytes = (p.n * kBM * 4 + 1023) / 1024 * 1024;
@@ -1061,8 +1047,8 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
       // update lists (draft, then verify; first occurrence) -- a superset of the
       // ids entering I, known without waiting for the update; the rows of ids
       // that were already active are dropped at level 1
-      if (tid == 0) {
-        sh_g0 = ld_acquire(a.step_ctr);
+      if (tid == kLoaders) {  // the MMA warp: its release fence would stall a loader thread
+        sh_g0 = ld_relaxed_u32(a.step_ctr);  // compared against later; the wait acquires
         red_add_release(a.arrive_ctr, 1u);
       }
       const int nu = fused_unique_ids(a, reinterpret_cast<int32_t*>(smem), (tile - a.tps_reg) * kBM, ids_s);
@@ -1076,9 +1062,11 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
       if (tid < kBM * UT)
         ids_s[tid] = row0 + tid < p.max_ids ? __ldcg(p.ids_base + (long long)seq * p.ids_stride + row0 + tid) : 0;
       if (tid == kBM * UT) sh_m = clamp_nact(p, seq);
-      if (MODE == kModeFused && tid == kBM + 1) sh_g0 = ld_acquire(a.step_ctr);  // same round trip
+      if (MODE == kModeFused && tid == kBM + 1) sh_g0 = ld_relaxed_u32(a.step_ctr);  // same round trip
       __syncthreads();
-      if (MODE == kModeFused && tid == 0) red_add_release(a.arrive_ctr, 1u);  // pre-update ids / n_active read
+      // pre-update ids / n_active read: arrive from the MMA warp (its release
+      // fence would stall a loader thread and with it the first stage)
+      if (MODE == kModeFused && tid == kLoaders) red_add_release(a.arrive_ctr, 1u);
       m = sh_m;
     }
     if (tid == 0 && local == 0) trace_mark(p.trace, 7);  // ids + n_active in shared memory
@@ -1140,6 +1128,44 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
         }
       }
       if (tid == 0 && local == 0) trace_mark(p.trace, 3);  // all loads issued and landed
+      if (MODE == kModeFused && warp == kLoadWarps - 1) {
+        // while the last MMAs run: wait for the update's publication (long
+        // done by now) and build this tile's drop mask -- regular tiles: the
+        // stale-slot words; patch tiles: rows whose id is not in the entering
+        // list (a warp-wide membership scan by shuffles)
+        if (lane == 0) {
+          long long spins = 0;
+          while (ld_acquire(a.step_ctr) == sh_g0)
+            if (++spins > kSpinLimit) __trap();
+        }
+        __syncwarp();
+        if (!patch_rows) {
+          if (lane < kBM / 32) sh_stale[lane] = __ldcg(&a.stale[(row0 >> 5) + lane]);
+        } else {
+          const int ne = __ldcg(&a.enter_meta[0]);
+          int32_t mid[4];
+          bool found[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) { mid[i] = ids_s[4 * lane + i]; found[i] = false; }
+          for (int base = 0; base < ne; base += 64) {  // up to 64 entering ids per round trip
+            const int32_t e0 = base + lane < ne ? __ldcg(&a.enter_ids[base + lane]) : -1;
+            const int32_t e1 = base + 32 + lane < ne ? __ldcg(&a.enter_ids[base + 32 + lane]) : -1;
+            for (int j = 0; j < 32; ++j) {
+              const int32_t x0 = __shfl_sync(0xffffffffu, e0, j), x1 = __shfl_sync(0xffffffffu, e1, j);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) found[i] = found[i] || x0 == mid[i] || x1 == mid[i];
+            }
+          }
+          uint32_t nib = 0u;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (4 * lane + i < rows && !found[i]) nib |= 1u << i;
+          uint32_t w = nib << ((lane & 7) * 4);
+#pragma unroll
+          for (int o = 1; o < 8; o <<= 1) w |= __shfl_xor_sync(0xffffffffu, w, o);
+          if ((lane & 7) == 0) sh_stale[lane >> 3] = w;
+        }
+      }
       // ---------------- epilogue: TMEM -> registers -> this unit's slot of P
       mbar_wait(smem_u32(&bars[2 * C::kStages]), local & 1);
       tc_fence_after();
@@ -1202,17 +1228,6 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
         }
         __syncwarp();
       }
-      if (MODE == kModeFused && !patch_rows) {
-        // meanwhile (drain in progress): the update's publication and this
-        // tile's stale-slot words, off the tail's critical path
-        if (lane == 0) {
-          long long spins = 0;
-          while (ld_acquire(a.step_ctr) == sh_g0)
-            if (++spins > kSpinLimit) __trap();
-        }
-        __syncwarp();
-        if (lane < kBM / 32) sh_stale[lane] = __ldcg(&a.stale[(row0 >> 5) + lane]);
-      }
       // the MMA warp waits until the epilogue has drained TMEM
       mbar_wait(smem_u32(&bars[2 * C::kStages + 1]), local & 1);
     }
@@ -1230,7 +1245,7 @@ __global__ void __launch_bounds__(kThreads, 1) head_tc_kernel(TcArgs a) {
   if (tid == 0) trace_mark(p.trace, 9);  // drained
   if (MODE == kModeFused) asm volatile("griddepcontrol.launch_dependents;");  // late trigger
   if (MODE == kModeFused) {
-    if (patch_rows || local == 0) wait_published(a, sh_g0);  // regular tiles: the MMA warp already did
+    if (local <= 0) wait_published(a, sh_g0);  // streaming CTAs: loader warp 15 already did
     if (tid == 0) trace_mark(p.trace, 12);  // publication seen
     if (local != 0)
       fused_tail(a, first, split, ids_s, local < 0 ? 0 : sh_m, reinterpret_cast<const float*>(smem),

@@ -87,6 +87,12 @@ def main():
                 continue
             rel = (col - t0) / 1e3
             print(f"  {name:13s} n={len(col):3d}  min {rel.min():7.2f}  med {np.median(rel):7.2f}  max {rel.max():7.2f} us")
+        if args.step and t.shape[0] > 125:  # fused: the patch cluster (CTAs 120-124) and the update cluster
+            for b0, label in ((120, "patch"), (125, "update")):
+                sel = t[b0:b0 + 5]
+                vals = {name: (sel[:, e][sel[:, e] > 0] - t0).max() / 1e3 for e, name in enumerate(EVENTS)
+                        if (sel[:, e] > 0).any()}
+                print(f"  {label} cluster (max over its CTAs):", {k: round(v, 2) for k, v in vals.items()})
 
 
 def trace_state():
