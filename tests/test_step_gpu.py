@@ -221,3 +221,28 @@ def test_step_host_buffers(cuda_ok, llama):
         ids = _check_state(st, ref, f"host step {s}")
         v, i, l = io.results()
         _check_head(v.unsqueeze(0), i.unsqueeze(0), l.unsqueeze(0), ids, Wb, H, k, f"host step {s}")
+
+
+def test_step_qwen_shape(cuda_ok):
+    """configs[2] shape (V = 152064, d = 3584): a 2k-token prompt with K_pre = 3,
+    then fused steps on the natural active set."""
+    from paper_2605_26444_b200 import ActiveVocab, HeadOutputs, step, step_is_fused
+    W = SI.bf16_weights(SI.QWEN["vocab"], SI.QWEN["d_model"], seed=0, device="cuda")
+    Wb = SI.bf16_bits(W)
+    V, d = W.shape
+    Wm, n, k = 3072, 60, 10
+    z = SI.Zipf(V)
+    prompt, pre = SI.prompt_and_prefill(z, 1, 2048, 3)
+    st = ActiveVocab(V, Wm)
+    st.init(0, _t(prompt), _t(pre))
+    assert step_is_fused(st, 60, 3, d, n, k)
+    ref = O.OracleStream(V, Wm).init(prompt, pre)
+    out = HeadOutputs(1, n, k, Wm, "cuda")
+    for s, (dd, vv) in enumerate(SI.decode_steps(z, 7, 6)):
+        H = SI.bf16_hidden(n, d, seed=600 + s, device="cuda")
+        v, i, l = step(st, 0, _t(dd), _t(vv), W, H, k, out=out)
+        ref.update(dd, vv)
+        if s in (0, 5):
+            torch.cuda.synchronize()
+            ids = _check_state(st, ref, f"qwen step {s}")
+            _check_head(v, i, l, ids, Wb, H, k, f"qwen fused step {s}")
