@@ -246,3 +246,69 @@ def test_step_qwen_shape(cuda_ok):
             torch.cuda.synchronize()
             ids = _check_state(st, ref, f"qwen step {s}")
             _check_head(v, i, l, ids, Wb, H, k, f"qwen fused step {s}")
+
+
+def test_step_other_sequence_of_a_batch(cuda_ok, llama):
+    """nanospec_step on sequence 3 of a 5-sequence state: only that sequence's
+    state changes; its top-k matches the oracle."""
+    from paper_2605_26444_b200 import ActiveVocab, step
+    W, Wb = llama
+    V, d = W.shape
+    Wm, n, k, B = 3072, 60, 10, 5
+    z = SI.Zipf(V)
+    st = ActiveVocab(V, Wm, batch=B)
+    refs = []
+    for b in range(B):
+        p, pre = SI.prompt_and_prefill(z, 40 + b, 500 + 100 * b, 3)
+        st.init(b, _t(p), _t(pre))
+        refs.append(O.OracleStream(V, Wm).init(p, pre))
+    before = [st.read(b)["ids"].copy() for b in range(B)]
+    for s, (dd, vv) in enumerate(SI.decode_steps(z, 41, 3)):
+        H = SI.bf16_hidden(n, d, seed=700 + s, device="cuda")
+        v, i, l = step(st, 3, _t(dd), _t(vv), W, H, k)
+        torch.cuda.synchronize()
+        refs[3].update(dd, vv)
+        got = st.read(3)
+        ids, _ = refs[3].active()
+        assert np.array_equal(got["ids"], ids), f"seq 3 step {s}"
+        _check_head(v, i, l, ids, Wb, H, k, f"batch seq 3 step {s}")
+    for b in (0, 1, 2, 4):
+        assert np.array_equal(st.read(b)["ids"], before[b]), f"sequence {b} must be untouched"
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_step_vocab_parallel_shards(cuda_ok, G):
+    """The fused step on vocab shards (rank r owns ids g % G == r, rows W[r::G]),
+    simulated on one GPU: every shard's state is bit-exact vs the oracle's shard
+    and the merged per-shard top-k / lse equal the oracle's over the full set."""
+    from paper_2605_26444_b200 import ActiveVocab, HeadOutputs, merge_topk, step, step_is_fused
+    V, d, Wm, n, k = 40000, 1024, 3072, 60, 10
+    W = SI.bf16_weights(V, d, seed=7, device="cuda")
+    Wb = SI.bf16_bits(W)
+    z = SI.Zipf(V)
+    p, pre = SI.prompt_and_prefill(z, 4, 3000, 3)
+    sts = []
+    for r in range(G):
+        st = ActiveVocab(V, Wm, shard_rank=r, n_shards=G)
+        st.init(0, _t(p), _t(pre))
+        sts.append(st)
+    assert step_is_fused(sts[0], 60, 3, d, n, k)  # the sharded state takes the one-launch path
+    ref = O.OracleStream(V, Wm).init(p, pre)
+    Ws = [W[r::G].contiguous() for r in range(G)]
+    outs = [HeadOutputs(1, n, k, Wm, "cuda") for _ in range(G)]
+    for s, (dd, vv) in enumerate(SI.decode_steps(z, 5, 4)):
+        H = SI.bf16_hidden(n, d, seed=800 + s, device="cuda")
+        res = [step(sts[r], 0, _t(dd), _t(vv), Ws[r], H, k, out=outs[r]) for r in range(G)]
+        ml, mi, mlse = merge_topk(torch.stack([x[0][0] for x in res]), torch.stack([x[1][0] for x in res]),
+                                  torch.stack([x[2][0] for x in res]), k)
+        torch.cuda.synchronize()
+        ref.update(dd, vv)
+        for r in range(G):
+            ids_r, bm_r = ref.active(r, G)
+            got = sts[r].read(0)
+            assert np.array_equal(got["ids"], ids_r) and np.array_equal(got["bitmap"], bm_r), f"shard {r} step {s}"
+        ids, _ = ref.active()
+        z_ref, A = O.logits(Wb, SI.bf16_bits(H), ids)
+        v_ref, id_ref = O.topk(z_ref, ids, k)
+        check_topk(ml.cpu().numpy(), mi.cpu().numpy(), z_ref, A, ids, v_ref, id_ref, f"vp G={G} step {s}")
+        check_lse(mlse.cpu().numpy(), O.lse(z_ref), f"vp G={G} step {s}")
