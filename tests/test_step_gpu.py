@@ -312,3 +312,25 @@ def test_step_vocab_parallel_shards(cuda_ok, G):
         v_ref, id_ref = O.topk(z_ref, ids, k)
         check_topk(ml.cpu().numpy(), mi.cpu().numpy(), z_ref, A, ids, v_ref, id_ref, f"vp G={G} step {s}")
         check_lse(mlse.cpu().numpy(), O.lse(z_ref), f"vp G={G} step {s}")
+
+
+def test_step_rule_r2_falls_back(cuda_ok, llama):
+    """Rule R2 (unique-FIFO) has no fused path: nanospec_step runs update + head
+    and still matches the oracle."""
+    from paper_2605_26444_b200 import ActiveVocab, step, step_is_fused
+    W, Wb = llama
+    V, d = W.shape
+    Wm, n, k = 1024, 16, 10
+    z = SI.Zipf(V)
+    p, pre = SI.prompt_and_prefill(z, 6, 800, 3)
+    st = ActiveVocab(V, Wm, rule="unique_fifo")
+    st.init(0, _t(p), _t(pre))
+    assert not step_is_fused(st, 60, 3, d, n, k)
+    ref = O.OracleStream(V, Wm, O.RULE_UNIQUE_FIFO).init(p, pre)
+    for s, (dd, vv) in enumerate(SI.decode_steps(z, 8, 3)):
+        H = SI.bf16_hidden(n, d, seed=900 + s, device="cuda")
+        v, i, l = step(st, 0, _t(dd), _t(vv), W, H, k)
+        torch.cuda.synchronize()
+        ref.update(dd, vv)
+        ids = _check_state(st, ref, f"R2 step {s}")
+        _check_head(v, i, l, ids, Wb, H, k, f"R2 step {s}")
