@@ -429,7 +429,7 @@ nanospec_status nanospec_debug_set_trace(unsigned long long* d_buf, int32_t ctas
 }
 
 nanospec_status nanospec_debug_set_head_mode(int32_t mode) {
-  if (mode < -1 || mode > 4) return NANOSPEC_EINVAL;
+  if (mode < -1 || mode > 6 || mode == 5) return NANOSPEC_EINVAL;
   set_head_tc_mode(mode);
   return NANOSPEC_OK;
 }

@@ -46,6 +46,7 @@
 #include "common.cuh"
 #include "internal.h"
 #include "state_fast.cuh"
+#include "tc_ptx.cuh"
 
 namespace nanospec {
 
@@ -75,6 +76,7 @@ constexpr int kModeFinishWide = 5;  // the same with two row tiles per unit (cap
 constexpr int kModePoll = 1;     // one unit per CTA, split-K partials + lists handed over through L2
 constexpr int kModeCluster = 2;  // one unit per CTA, the S splits of a tile form a cluster (DSMEM reduction)
 constexpr int kModeFused = 3;    // cluster mode + the state update in the same launch (patch tiles)
+constexpr int kModePair = 6;     // opt-in: the pair-split kernel of head_pair.cu
 constexpr int kMaxCluster = 8;   // portable cluster size
 constexpr int kMaxL2Lists = 160;  // poll mode: tiles per sequence (5 lists per lane at level 2)
 constexpr long long kSpinLimit = 1ll << 26;  // polls before giving up (a trap beats a hung GPU)
@@ -106,136 +108,6 @@ struct TcArgs {
 
 // ------------------------------------------------------------------ PTX helpers
 // ------------------------------------------------------------------ PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(bar), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-// K-major, 128B-swizzled UMMA shared-memory descriptor (SM100): start>>4
-// [0,14), LBO>>4 [16,30) (unused for SW128 K-major: 1), SBO>>4 [32,46) = 1024 B
-// between 8-row groups, version 1 at [46,48), layout SWIZZLE_128B (2) at [61,64).
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1u << 16) | ((uint64_t)(1024u >> 4) << 32) |
-         ((uint64_t)1u << 46) | ((uint64_t)2u << 61);
-}
-// Instruction descriptor, kind::f16: D fp32 [4,6)=1, A bf16 [7,10)=1, B bf16
-// [10,13)=1, both K-major, N>>3 at [17,23), M>>4 at [24,29).
-__host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                          uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-__device__ __forceinline__ void umma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-               : "memory");
-}
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-__device__ __forceinline__ uint32_t ld_acquire(const unsigned* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
-  unsigned old;
-  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
-}
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ uint4 ld_relaxed_v4(const void* p) {
-  uint4 v;
-  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ uint2 ld_relaxed_v2(const void* p) {
-  uint2 v;
-  asm volatile("ld.relaxed.gpu.global.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed_f32(float* p, float v) {
-  asm volatile("st.relaxed.gpu.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
-}
-__device__ __forceinline__ void st_relaxed_v2(uint2* p, uint2 v) {
-  asm volatile("st.relaxed.gpu.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
-}
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// Address of the same shared-memory location in CTA `rank` of the cluster.
-__device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ float4 ld_dsmem_v4(uint32_t caddr) {
-  float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(caddr)
-               : "memory");
-  return v;
-}
-__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v);
-__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void red_add_release(unsigned* p, unsigned v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ int clamp_nact(const HeadProblem& p, int b) {
-  int m = p.nact_base[(long long)b * p.nact_stride];
-  return m < 0 ? 0 : (m > p.max_ids ? p.max_ids : m);
-}
 
 template <int NT, int UT = 1>  // UT: 128-row tiles per work unit (the persistent finisher mode takes 2)
 struct Cfg {
@@ -252,21 +124,6 @@ struct Cfg {
   static constexpr int kColGroups = NT / 16 < 4 ? NT / 16 : 4;  // epilogue column groups
 };
 
-__device__ __forceinline__ float key_value(uint32_t kk) {
-  if (kk == 0u) return -INFINITY;  // "none"
-  return __uint_as_float((kk & 0x80000000u) ? (kk & 0x7fffffffu) : ~kk);
-}
-// (value desc, id asc): a before b
-__device__ __forceinline__ bool key_before(uint32_t ka, uint32_t ga, uint32_t kb, uint32_t gb) {
-  return ka > kb || (ka == kb && ga < gb);
-}
-// Compare-exchange: afterwards entry a precedes entry b in (value desc, id asc).
-__device__ __forceinline__ void cx(uint32_t& ka, uint32_t& ga, uint32_t& kb, uint32_t& gb) {
-  if (key_before(kb, gb, ka, ga)) {
-    const uint32_t tk = ka; ka = kb; kb = tk;
-    const uint32_t tg = ga; ga = gb; gb = tg;
-  }
-}
 // Sort 8 entries (19-comparator network).
 __device__ __forceinline__ void sort8(uint32_t (&k)[kFinRows], uint32_t (&g)[kFinRows]) {
 #define NS_CX(i, j) cx(k[i], g[i], k[j], g[j])
@@ -300,13 +157,6 @@ __device__ __forceinline__ uint2 warp_select(uint32_t (&k)[L], uint32_t (&g)[L],
     }
   }
   return mine;
-}
-// Online lse partial: fold (m2, e2) into (m, e), e = sum exp(z - m).
-__device__ __forceinline__ void lse_fold(float& m, float& e, float m2, float e2) {
-  if (m2 == -INFINITY) return;
-  if (m == -INFINITY) { m = m2; e = e2; return; }
-  if (m2 > m) { e = e * __expf(m - m2) + e2; m = m2; }
-  else e += e2 * __expf(m2 - m);
 }
 
 // Finisher of one (sequence, node): logits of the m active rows = sum of the S
@@ -420,35 +270,6 @@ __device__ void finish_node(const TcArgs& a, int seq, int node, float* sp, int r
   __syncthreads();  // wl / wm free for the next pair
 }
 
-// k-th largest (1 <= k <= 32) of one key per lane, by counting (ties by lane).
-__device__ __forceinline__ uint32_t warp_kth_key(uint32_t x, int k) {
-  const int lane = threadIdx.x & 31;
-  int rank = 0;
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const uint32_t o = __shfl_sync(0xffffffffu, x, j);
-    rank += (o > x || (o == x && j < lane)) ? 1 : 0;
-  }
-  const unsigned sel = __ballot_sync(0xffffffffu, rank == k - 1);
-  return __shfl_sync(0xffffffffu, x, __ffs(sel) - 1);
-}
-// Rank `cnt` staged (key, gid) candidates by counting (all loads independent)
-// and write the k best, best first, to out[0..k).
-__device__ __forceinline__ void warp_rank_write(const uint2* cs, int cnt, int k, uint2* out) {
-  const int lane = threadIdx.x & 31;
-  for (int e = lane; e < cnt; e += 32) {
-    const uint2 me = cs[e];
-    int r = 0;
-    for (int f = 0; f < cnt; ++f) {
-      const uint2 o = cs[f];
-      r += key_before(o.x, o.y, me.x, me.y) ? 1 : 0;
-    }
-    if (r < k) out[r] = me;
-  }
-}
-// Threshold selection of a warp's top-k from 4 entries per lane (unsorted):
-// T = k-th largest lane maximum (k lanes each own an entry >= T, so every
-// top-k entry is >= T); the entries >= T are compacted into `scratch` and
 // ranked by counting.  Returns this lane's entry of the sorted top-k.
 __device__ __forceinline__ uint2 warp_topk_thr(const uint32_t (&key)[4], const uint32_t (&gid)[4], int k,
                                                uint2* scratch) {
@@ -736,9 +557,6 @@ __device__ void poll_tail(const TcArgs& a, int tile, int split, const int32_t* i
 // compacted (warp scan) and the candidates are ranked by counting.  Scratch:
 // ntiles * (2k + 1) + k entries.  List t comes from tile t (t < nreg), else
 // from tile treg + t - nreg (the fused step's patch tiles).
-__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
-}
 __device__ void level2_thr(const TcArgs& a, int seq, int node, int ntiles, uint2* scratch, int nreg = 1 << 30,
                            int treg = 0) {
   const HeadProblem& p = a.p;
@@ -1308,7 +1126,7 @@ int g_cluster_cap = 0;  // debug: largest cluster (K-split) size tried, 0 = kMax
 int g_fused_pdl = 0;  // (PDL with the trigger moved after the stream also faulted: kept off)
 
 struct ScratchLayout {
-  size_t grid_word, node_ctr, part, cand, step_ctr, arrive_ctr, stale, enter_ids, enter_meta, total;
+  size_t grid_word, node_ctr, part, cand, step_ctr, arrive_ctr, stale, enter_ids, enter_meta, pcand, total;
 };
 constexpr int kMaxPatchTiles = kFastThreads / kBM;  // fused step: entering ids <= kFastThreads
 
@@ -1329,6 +1147,7 @@ inline ScratchLayout scratch_layout(int batch, int max_ids, int n) {
   L.stale = off;     off += al(sizeof(uint32_t) * (size_t)((max_ids + 31) / 32));
   L.enter_ids = off; off += al(sizeof(int32_t) * kFastThreads);
   L.enter_meta = off; off += al(sizeof(int) * 4);
+  L.pcand = off;     off += al(pair_cand_bytes(n));  // head_pair.cu level-1 lists
   L.total = off;
   return L;
 }
@@ -1573,9 +1392,32 @@ size_t head_tc_scratch_bytes(int batch, int max_ids, int n) { return scratch_lay
 void set_head_tc_mode(int mode) { g_head_mode = mode; }
 void set_head_tc_cluster_cap(int s) { g_cluster_cap = s; }
 
+PairScratch pair_scratch(void* scratch, const ScratchLayout& L) {
+  char* sc = (char*)scratch;
+  PairScratch s;
+  s.cand = (uint2*)(sc + L.pcand);
+  s.node_ctr = (unsigned*)(sc + L.node_ctr);
+  s.grid_word = (unsigned*)(sc + L.grid_word);
+  s.step_ctr = (unsigned*)(sc + L.step_ctr);
+  s.arrive_ctr = (unsigned*)(sc + L.arrive_ctr);
+  s.stale = (uint32_t*)(sc + L.stale);
+  s.enter_ids = (int32_t*)(sc + L.enter_ids);
+  s.enter_meta = (int*)(sc + L.enter_meta);
+  return s;
+}
+
 cudaError_t launch_step_tc(const HeadProblem& p, const AppendArgs& upd, int k, float* topk_logit, int32_t* topk_id,
                            float* lse, void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t stream,
                            bool dry_run) {
+  if (g_head_mode == kModePair) {  // opt-in: the pair-split kernel (head_pair.cu)
+    const ScratchLayout L = scratch_layout(1, p.max_ids, p.n);
+    if (dry_run || L.total <= scratch_bytes) {
+      const cudaError_t e = launch_step_pair(p, upd, k, topk_logit, topk_id, lse,
+                                             dry_run ? PairScratch{} : pair_scratch(scratch, L), num_sms, stream,
+                                             dry_run);
+      return e;
+    }
+  }
   if (p.batch != 1 || p.d % kBK != 0 || p.n < 1 || p.n > 256 || p.ldw % 8 != 0 || k < 1 || k > kMaxK)
     return cudaErrorNotSupported;
 #define NS_STEP(NTV) \
@@ -1590,6 +1432,11 @@ cudaError_t launch_step_tc(const HeadProblem& p, const AppendArgs& upd, int k, f
 
 cudaError_t launch_head_tc(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse,
                            void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t stream) {
+  if (g_head_mode == kModePair) {  // opt-in: the pair-split kernel (head_pair.cu)
+    const ScratchLayout L = scratch_layout(p.batch, p.max_ids, p.n);
+    if (L.total > scratch_bytes) return cudaErrorInvalidValue;
+    return launch_head_pair(p, k, topk_logit, topk_id, lse, pair_scratch(scratch, L), num_sms, stream);
+  }
   if (p.d % kBK != 0 || p.n < 1 || p.n > 256 || p.ldw % 8 != 0 || k < 1 || k > kMaxK) return cudaErrorNotSupported;
   if (p.n <= 16) return launch_nt<16>(p, k, topk_logit, topk_id, lse, scratch, scratch_bytes, num_sms, stream);
   if (p.n <= 32) return launch_nt<32>(p, k, topk_logit, topk_id, lse, scratch, scratch_bytes, num_sms, stream);

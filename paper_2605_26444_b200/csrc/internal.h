@@ -50,6 +50,26 @@ struct AppendArgs;
 cudaError_t launch_step_tc(const HeadProblem& p, const AppendArgs& upd, int k, float* topk_logit, int32_t* topk_id,
                            float* lse, void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t stream,
                            bool dry_run = false);
+// Pair-split tensor-core head (head_pair.cu): the one-wave regime (every row
+// tile resident at once).  Scratch shared with head_tc.cu's layout.
+constexpr int kMaxPairSMs = 256;
+struct PairScratch {
+  uint2* cand;          // pair_cand_bytes(n): row keys, ids, tile maxima and lse partials
+  unsigned* node_ctr;   // [batch * n], zero between launches
+  unsigned* grid_word;  // grid barrier word (generation << 12 | arrivals), shared with head_tc.cu
+  unsigned* step_ctr;   // fused: publication generation
+  unsigned* arrive_ctr; // fused: zero between launches
+  uint32_t* stale;      // fused: [max_ids / 32]
+  int32_t* enter_ids;   // fused: [kFastThreads]
+  int* enter_meta;      // fused: [4]
+};
+size_t pair_cand_bytes(int n);
+cudaError_t launch_head_pair(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse,
+                             const PairScratch& s, int num_sms, cudaStream_t stream);
+cudaError_t launch_step_pair(const HeadProblem& p, const AppendArgs& upd, int k, float* topk_logit,
+                             int32_t* topk_id, float* lse, const PairScratch& s, int num_sms, cudaStream_t stream,
+                             bool dry_run);
+void set_head_pair_enabled(int on);
 // Whether launch_state_append would take the per-step fast path for these lists.
 bool state_fast_path(const StateView& sv, int reset, long long a_len, int a_dedup, long long b_len, int b_dedup);
 // Debug: force the fused head's reduction mode (-1 auto, 0 finisher, 1 poll, 2 cluster).
