@@ -136,11 +136,20 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- reference arm (CPU oracle)
-def cpu_oracle_steps(cfg, n_nodes, k, steps, seed=0):
+def cpu_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_oracle_steps(cfg, n_nodes, k, steps, seed=0, cores=1):
     """Runs `steps` full oracle steps (state update by Eq. 4/5 over the retained
     window + fp64 restricted head + top-k + lse) on the host; returns us/step and
-    a description.  The oracle is used as it stands (single-threaded C)."""
-    import torch
+    a description.  The oracle is used as it stands (single-threaded C); with
+    cores > 1 the head of each step is split by draft-tree node over that many
+    threads (the C calls release the GIL), the state update stays serial."""
+    from concurrent.futures import ThreadPoolExecutor
 
     from oracle import oracle as O
     from synthetic import inputs as SI
@@ -151,16 +160,27 @@ def cpu_oracle_steps(cfg, n_nodes, k, steps, seed=0):
     Wb = SI.bf16_bits(Wt)
     H = SI.bf16_bits(SI.bf16_hidden(n_nodes, d, seed=1))
     ref = O.OracleStream(V, Wm).init(prompt)
-    t0 = time.perf_counter()
-    for dr, vr in ups:
-        ref.update(dr, vr)
-        ref.S = ref.S[-Wm:]  # only the window matters for Eq. 5; keeps the host stream bounded
-        ids, _ = ref.active()
-        z, _ = O.logits(Wb, H, ids, want_abs=False)
+    cores = max(1, min(cores, n_nodes))
+    bounds = [(n_nodes * c // cores, n_nodes * (c + 1) // cores) for c in range(cores)]
+
+    def head(ids, lo, hi):
+        z, _ = O.logits(Wb, H[lo:hi], ids, want_abs=False)
         O.topk(z, ids, k)
         O.lse(z)
-    dt = time.perf_counter() - t0
-    return dt / steps * 1e6, f"{steps} full steps (|I|={len(ids)}, n={n_nodes}, k={k}) of the {cfg['model']} workload"
+
+    with ThreadPoolExecutor(max_workers=cores) as ex:
+        t0 = time.perf_counter()
+        for dr, vr in ups:
+            ref.update(dr, vr)
+            ref.S = ref.S[-Wm:]  # only the window matters for Eq. 5; keeps the host stream bounded
+            ids, _ = ref.active()
+            if cores == 1:
+                head(ids, 0, n_nodes)
+            else:
+                list(ex.map(lambda b: head(ids, *b), bounds))
+        dt = time.perf_counter() - t0
+    return dt / steps * 1e6, (f"{steps} full steps (|I|={len(ids)}, n={n_nodes}, k={k}) of the {cfg['model']} "
+                              f"workload, head split by node over {cores} thread(s)")
 
 
 def run_reference(args):
@@ -173,15 +193,16 @@ def run_reference(args):
         return
     cfg = CONFIGS[args.config]
     n = args.n_nodes
-    t_one, _ = cpu_oracle_steps(cfg, n, args.k, 1)
+    cores = cpu_cores()
+    t_one, _ = cpu_oracle_steps(cfg, n, args.k, 1, cores=cores)
     budget_us = 120e6
     steps = max(1, args.steps)
     n_s = n
     if (steps + args.warmup) * t_one > budget_us:
         n_s = max(1, int(n * budget_us / ((steps + args.warmup) * t_one)))
     if args.warmup:
-        cpu_oracle_steps(cfg, n_s, args.k, min(args.warmup, 3))
-    us, sample = cpu_oracle_steps(cfg, n_s, args.k, steps)
+        cpu_oracle_steps(cfg, n_s, args.k, min(args.warmup, 3), cores=cores)
+    us, sample = cpu_oracle_steps(cfg, n_s, args.k, steps, cores=cores)
     us = us * n / n_s
     if n_s != n:
         sample += f"; {n_s} of {n} nodes per step, time scaled x{n / n_s:.2f}"
@@ -191,7 +212,8 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
         "config": {"workload": f"{cfg['model']} draft head: V={cfg['vocab']} d={cfg['d']} |I|={cfg['w_max']} "
                                f"n={n} k={args.k} batch=1"},
-        "cpu_baseline": {"value": round(us, 1), "unit": "us/step", "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": round(us, 1), "unit": "us/step", "cores": min(cores, n_s), "kind": "oracle",
+                         "sample": sample},
         "e2e": {"value": round(us, 1), "unit": "us/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -461,8 +483,12 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and not args.no_cpu:
-        us_cpu, sample = cpu_oracle_steps(cfg, n, k, args.cpu_sample_steps)
-        cpu = {"value": round(us_cpu, 1), "unit": "us/step", "cores": 1, "kind": "oracle", "sample": sample}
+        # the oracle as it stands on every host core (head split by node), and on one core
+        cores = min(cpu_cores(), n)
+        us_cpu, sample = cpu_oracle_steps(cfg, n, k, args.cpu_sample_steps, cores=cores)
+        us_cpu1, _ = cpu_oracle_steps(cfg, n, k, 1, cores=1)
+        cpu = {"value": round(us_cpu, 1), "unit": "us/step", "cores": cores, "kind": "oracle", "sample": sample,
+               "single_core_value": round(us_cpu1, 1)}
 
     launches_per_step = 1 if fused else (3 if args.head == "simt" else 2)  # fused step | update + head (+ select)
     value = ms_total * 1e3 / (K * world)
@@ -672,8 +698,29 @@ def run_vp32k(args):
         dist.destroy_process_group()
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def _spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: re-launch this command as N ranks
+    (one process per GPU, the driver's own launch form) and pass rank 0's line on."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_spawn_ranks(args.gpus))
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        # communicator set-up in the log (nranks, NVLS / P2P transport) so the rank count can be checked
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if args.impl == "reference":
         run_reference(args)
     elif args.config == "dp64":

@@ -230,6 +230,22 @@ nanospec_status nanospec_step(nanospec_state st, int32_t seq, const int32_t* d_d
                               int32_t* d_topk_id, float* d_lse, void* d_scratch, size_t scratch_bytes,
                               cudaStream_t stream);
 
+/* nanospec_step that also writes the logits of every row the fused launch
+ * streamed (tests: the fused launch's contraction checked element by element).
+ *   d_debug_logits fp32 [n_nodes x (w_max + n_draft + k_ver)], row i:
+ *     columns [0, w_max)          the PRE-update slots ids[0, n_old) (n_old = |I|
+ *                                 before the step; later columns unspecified);
+ *     columns [w_max, w_max + e)  the update-list entries, draft then verify.
+ *   Only the rows in the updated active set feed the top-k / lse (the others
+ *   are rows whose id left I, repeats, or ids that were already active).
+ * EUNSUPPORTED when the step cannot run as one fused launch (then nothing is
+ * done); otherwise exactly nanospec_step. */
+nanospec_status nanospec_step_debug(nanospec_state st, int32_t seq, const int32_t* d_draft_ids, int32_t n_draft,
+                                    const int32_t* d_verify_topk, int32_t k_ver, const void* d_w_head,
+                                    int32_t d_model, int64_t ldw, const void* d_hidden, int32_t n_nodes, int32_t k,
+                                    float* d_topk_logit, int32_t* d_topk_id, float* d_lse, float* d_debug_logits,
+                                    void* d_scratch, size_t scratch_bytes, cudaStream_t stream);
+
 /* nanospec_step with HOST buffers (the end-to-end call): one host->device copy
  * of the packed inputs, the step, one device->host copy of the packed results,
  * all asynchronous on `stream` (pinned host memory for real overlap).

@@ -21,11 +21,12 @@ from .nanospec import (  # noqa: E402
     state_workspace_bytes,
     StepHostIO,
     step,
+    step_debug,
     step_host,
     step_is_fused,
 )
 
 __all__ = [
     "ActiveVocab", "HeadOutputs", "draft_logits_topk", "logits_topk_ids", "merge_topk",
-    "head_scratch_bytes", "state_workspace_bytes", "step", "step_host", "StepHostIO", "step_is_fused",
+    "head_scratch_bytes", "state_workspace_bytes", "step", "step_debug", "step_host", "StepHostIO", "step_is_fused",
 ]

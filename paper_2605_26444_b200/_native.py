@@ -22,7 +22,7 @@ EXPORTS = [
     "nanospec_state_read", "nanospec_state_check", "nanospec_state_ids_ptr", "nanospec_state_n_active_ptr",
     "nanospec_head_scratch_bytes", "nanospec_draft_logits_topk", "nanospec_draft_logits_topk_ex",
     "nanospec_logits_topk_ids", "nanospec_merge_topk", "nanospec_debug_set_trace",
-    "nanospec_debug_set_head_mode", "nanospec_step", "nanospec_step_fused",
+    "nanospec_debug_set_head_mode", "nanospec_step", "nanospec_step_fused", "nanospec_step_debug",
     "nanospec_debug_set_cluster_cap", "nanospec_step_host", "nanospec_step_host_io_bytes",
 ]
 
@@ -77,6 +77,8 @@ def lib():
     L.nanospec_step_host.argtypes = [vp, i32, vp, i32, i32, vp, i32, i64, i32, i32, vp, vp, sz, vp, sz, vp]
     L.nanospec_step_fused.argtypes = [vp, i32, i32, i32, i32, i32]
     L.nanospec_step.argtypes = [vp, i32, vp, i32, vp, i32, vp, i32, i64, vp, i32, i32, vp, vp, vp, vp, sz, vp]
+    L.nanospec_step_debug.argtypes = [vp, i32, vp, i32, vp, i32, vp, i32, i64, vp, i32, i32, vp, vp, vp, vp, vp, sz,
+                                      vp]
     _lib = L
     return L
 

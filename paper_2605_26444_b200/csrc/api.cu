@@ -291,11 +291,12 @@ nanospec_status nanospec_draft_logits_topk(const nanospec_state st, const void* 
                                        d_lse, d_debug_logits, d_scratch, scratch_bytes, NANOSPEC_HEAD_AUTO, stream);
 }
 
-nanospec_status nanospec_step(nanospec_state st, int32_t seq, const int32_t* d_draft_ids, int32_t n_draft,
-                              const int32_t* d_verify_topk, int32_t k_ver, const void* d_w_head, int32_t d_model,
-                              int64_t ldw, const void* d_hidden, int32_t n_nodes, int32_t k, float* d_topk_logit,
-                              int32_t* d_topk_id, float* d_lse, void* d_scratch, size_t scratch_bytes,
-                              cudaStream_t stream) {
+namespace {
+nanospec_status step_impl(nanospec_state st, int32_t seq, const int32_t* d_draft_ids, int32_t n_draft,
+                          const int32_t* d_verify_topk, int32_t k_ver, const void* d_w_head, int32_t d_model,
+                          int64_t ldw, const void* d_hidden, int32_t n_nodes, int32_t k, float* d_topk_logit,
+                          int32_t* d_topk_id, float* d_lse, float* d_debug_logits, void* d_scratch,
+                          size_t scratch_bytes, cudaStream_t stream) {
   if (!st || seq < 0 || seq >= st->sv.batch || n_draft < 0 || k_ver < 0) return NANOSPEC_EINVAL;
   if ((n_draft > 0 && !d_draft_ids) || (k_ver > 0 && !d_verify_topk)) return NANOSPEC_EINVAL;
   if (!d_w_head || !d_hidden || !d_topk_logit || !d_topk_id) return NANOSPEC_EINVAL;
@@ -317,7 +318,7 @@ nanospec_status nanospec_step(nanospec_state st, int32_t seq, const int32_t* d_d
   hp.nact_stride = sizeof(Meta) / sizeof(int32_t);
   hp.max_ids = sv.w_max;
   hp.n_shards = sv.n_shards;
-  hp.logits = nullptr;
+  hp.logits = d_debug_logits;
   hp.trace = trace_buffer();
   if (state_fast_path(sv, 0, d_draft_ids ? n_draft : 0, 1, d_verify_topk ? k_ver : 0, 1)) {
     AppendArgs upd;
@@ -327,16 +328,41 @@ nanospec_status nanospec_step(nanospec_state st, int32_t seq, const int32_t* d_d
     upd.a = ListArg{d_draft_ids, d_draft_ids ? n_draft : 0, 0, 1};
     upd.b = ListArg{d_verify_topk, d_verify_topk ? k_ver : 0, 0, 1};
     const size_t lb = logits_bytes(1, sv.w_max, n_nodes);
-    cudaError_t e = launch_step_tc(hp, upd, k, d_topk_logit, d_topk_id, d_lse, (char*)d_scratch + lb,
-                                   scratch_bytes - lb, sm_count(), stream);
+    cudaError_t e = d_debug_logits
+                        ? launch_step_split_only(hp, upd, k, d_topk_logit, d_topk_id, d_lse, (char*)d_scratch + lb,
+                                                 scratch_bytes - lb, sm_count(), stream)
+                        : launch_step_tc(hp, upd, k, d_topk_logit, d_topk_id, d_lse, (char*)d_scratch + lb,
+                                         scratch_bytes - lb, sm_count(), stream);
     if (e == cudaSuccess) return NANOSPEC_OK;
     if (e != cudaErrorNotSupported) return NANOSPEC_ECUDA;
   }
+  if (d_debug_logits) return NANOSPEC_EUNSUPPORTED;  // the superset-row layout exists only in the fused launch
+  hp.logits = nullptr;
   // not fusable: the update, then the head on that sequence (two launches)
   nanospec_status r = nanospec_state_update(st, seq, d_draft_ids, n_draft, d_verify_topk, k_ver, stream);
   if (r != NANOSPEC_OK) return r;
   return run_head(hp, k, d_topk_logit, d_topk_id, d_lse, nullptr, d_scratch, scratch_bytes, NANOSPEC_HEAD_AUTO,
                   stream);
+}
+}  // namespace
+
+nanospec_status nanospec_step(nanospec_state st, int32_t seq, const int32_t* d_draft_ids, int32_t n_draft,
+                              const int32_t* d_verify_topk, int32_t k_ver, const void* d_w_head, int32_t d_model,
+                              int64_t ldw, const void* d_hidden, int32_t n_nodes, int32_t k, float* d_topk_logit,
+                              int32_t* d_topk_id, float* d_lse, void* d_scratch, size_t scratch_bytes,
+                              cudaStream_t stream) {
+  return step_impl(st, seq, d_draft_ids, n_draft, d_verify_topk, k_ver, d_w_head, d_model, ldw, d_hidden, n_nodes, k,
+                   d_topk_logit, d_topk_id, d_lse, nullptr, d_scratch, scratch_bytes, stream);
+}
+
+nanospec_status nanospec_step_debug(nanospec_state st, int32_t seq, const int32_t* d_draft_ids, int32_t n_draft,
+                                    const int32_t* d_verify_topk, int32_t k_ver, const void* d_w_head,
+                                    int32_t d_model, int64_t ldw, const void* d_hidden, int32_t n_nodes, int32_t k,
+                                    float* d_topk_logit, int32_t* d_topk_id, float* d_lse, float* d_debug_logits,
+                                    void* d_scratch, size_t scratch_bytes, cudaStream_t stream) {
+  if (!d_debug_logits) return NANOSPEC_EINVAL;
+  return step_impl(st, seq, d_draft_ids, n_draft, d_verify_topk, k_ver, d_w_head, d_model, ldw, d_hidden, n_nodes, k,
+                   d_topk_logit, d_topk_id, d_lse, d_debug_logits, d_scratch, scratch_bytes, stream);
 }
 
 size_t nanospec_step_host_io_bytes(int32_t n_nodes, int32_t d_model, int32_t n_draft, int32_t k_ver, int32_t k,
@@ -429,7 +455,7 @@ nanospec_status nanospec_debug_set_trace(unsigned long long* d_buf, int32_t ctas
 }
 
 nanospec_status nanospec_debug_set_head_mode(int32_t mode) {
-  if (mode < -1 || mode > 6 || mode == 5) return NANOSPEC_EINVAL;
+  if (mode < -1 || mode > 7 || mode == 5) return NANOSPEC_EINVAL;
   set_head_tc_mode(mode);
   return NANOSPEC_OK;
 }

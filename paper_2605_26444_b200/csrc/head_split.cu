@@ -1,0 +1,857 @@
+// a3+a4+a5 (and, for nanospec_step, a2) as TWO kernels chained by
+// programmatic dependent launch -- no CTA ever waits for another CTA of the
+// head path, so no launch needs the whole grid resident:
+//
+//   z'[b][i][j] = sum_c W[row(ids_b[j])][c] * H[b][i][c]     (Eq. 2 on I)
+//   then per (b, i) the top-k of z' by (value desc, id asc) + lse
+//
+// Kernel A (head_stream_kernel, 544 threads, one CTA per SM): the active rows
+// of a sequence are cut into 128-row tiles; every tile is split along K over
+// S CTAs (S = #SMs / #tiles: 6 at the headline, 24 tiles x 6 = 144 CTAs; S = 1
+// and a persistent loop over tiles when the tiles outnumber the SMs).  A CTA
+// gathers its tile's rows of W_head (16-byte cp.async straight from the
+// [V x d] weight into 128B-swizzled shared memory: no repack buffer, the
+// paper's P:247-258 design is prior art) and the hidden states' K slice,
+// one lane issues tcgen05.mma (M = 128 rows, N = NT >= n nodes, K = 16) into
+// TMEM, and the 16 loader warps drain the fp32 partial tile to L2 (one
+// 128-byte store per node per warp).  It then exits: nothing in A waits for
+// another CTA.
+//
+// Kernel B (head_select_kernel, one CTA per (sequence, node)): waits for A
+// (griddepcontrol.wait: A complete, its stores visible), sums every row's S
+// partials in K-chunk order (one order for every tile: equal rows give
+// bit-equal logits), keeps the row only if it is in I, folds the lse online,
+// and selects the top-k: each warp keeps a running sorted top-k list (a batch
+// of 128 rows enters through a threshold -- the k-th largest lane maximum --
+// so only a few candidates are ranked), then one warp merges the warp lists
+// (threshold = k-th largest list head, rank by counting).  Global ids come
+// from the row-id table A wrote, so B never reads the state.
+//
+// Fused step (nanospec_step, one sequence): A streams a SUPERSET of the
+// post-update active set that is known without waiting for the update -- the
+// pre-update slots ids[0, n_old) plus the raw update-list entries as "patch"
+// rows -- while its last CTA runs the O(changes) state update (state_fast.cuh).
+// The update writes a drop bitmap (pre-update slots whose id left I; patch
+// rows that are a repeat, invalid, or whose id was already active) and waits,
+// one way only, until every streaming CTA has read the pre-update slots
+// before it rewrites ids[] / pos[] / meta (the streaming CTAs never wait, so
+// this cannot deadlock whatever the residency).  B then drops those rows.
+// Result == update, then head.
+#include <cuda.h>
+#include <math.h>
+#include <stdlib.h>
+
+#include "common.cuh"
+#include "internal.h"
+#include "state_fast.cuh"
+#include "tc_ptx.cuh"
+
+namespace nanospec {
+
+namespace {
+
+constexpr int kBM = 128;           // rows per tile (UMMA M)
+constexpr int kBK = 64;            // K per stage: one 128-byte swizzle atom
+constexpr int kLW = 16;            // loader / drain warps
+constexpr int kLoaders = kLW * 32;
+constexpr int kAThreads = kLoaders + 32;  // + the MMA-issue warp
+constexpr int kBudget = 192 * 1024;
+constexpr int kMaxS = 32;          // K splits per tile
+constexpr int kMaxK = 32;
+constexpr long long kSpin = 1ll << 30;  // updater's arrival poll bound (a trap beats a hung GPU)
+
+template <int NT>
+struct ACfg {
+  static constexpr int kABytes = kBM * kBK * 2;   // 16 KB of W rows
+  static constexpr int kBBytes = NT * kBK * 2;    // NT x 128 B of H
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = (kBudget / kStageBytes) > 8 ? 8 : (kBudget / kStageBytes);
+  static constexpr int kTmemCols = NT < 32 ? 32 : NT;
+  static constexpr int kStageArea = kStages * kStageBytes;
+  static constexpr int kSmemBytes = kStageArea + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kColGroups = NT / 16 < 4 ? NT / 16 : 4;  // drain column groups
+};
+
+struct SplitArgs {
+  HeadProblem p;
+  float* part;          // [units][n][128] fp32 partial tiles
+  int32_t* rowgid;      // [batch * (tps + n_patch)][128] global id of every streamed row (-1: none)
+  int tps;              // regular tiles per sequence = ceil(max_ids / 128)
+  int n_patch;          // fused step: patch tiles (raw update-list entries, 128 per tile)
+  int ntiles;           // batch * tps + n_patch; global tile t: regular (t / tps, t % tps), then patch tiles
+  int S, extra;         // K splits: tiles t < extra take S + 1, the others S (every SM busy)
+  int units;            // sum of the tiles' splits
+  int heads;            // streaming CTAs (the fused grid has one more: the updater)
+  // fused step (batch 1)
+  AppendArgs upd;
+  int L;                // raw update-list entries (patch rows)
+  unsigned* arrive_ctr; // streaming CTAs that have read the pre-update slots (the updater re-zeroes it)
+  int* mrows;           // [batch] rows of the regular tiles (|I| as A read it), written by A's (tile 0, split 0) CTA
+  uint32_t* drop;       // [(tps + n_patch) * 4] rows that do not count, written by the updater
+  // outputs (B)
+  float* topk_logit;    // [batch][n][k]
+  int32_t* topk_id;
+  float* lse;           // [batch][n] or null
+  int k;
+  long long dbg_ld;     // debug logits: floats between the rows of one (sequence, node)
+  int trace_base;       // debug trace: B's CTA b writes trace row trace_base + b (after A's rows)
+  int w_evict_first;    // W rows streamed with an L2 evict-first policy
+};
+
+__device__ __forceinline__ void trace_b(const SplitArgs& a, int e) {
+  if (a.p.trace) a.p.trace[(long long)(a.trace_base + blockIdx.x) * kTraceSlots + e] = globaltimer();
+}
+
+// Unit u -> (sequence, tile within the sequence, split, splits of the tile, unit of split 0).
+struct Unit {
+  int seq, tile, split, S, base;
+};
+// Splits and first unit of global tile t.
+__device__ __forceinline__ void tile_units(const SplitArgs& a, int t, int& S, int& base) {
+  if (t < a.extra) { S = a.S + 1; base = t * S; }
+  else { S = a.S; base = a.extra * (a.S + 1) + (t - a.extra) * a.S; }
+}
+__device__ __forceinline__ int global_tile(const SplitArgs& a, int seq, int tile) {
+  return tile < a.tps ? seq * a.tps + tile : a.p.batch * a.tps + (tile - a.tps);
+}
+__device__ __forceinline__ Unit unit_of(const SplitArgs& a, int u) {
+  Unit r;
+  const int hi = a.extra * (a.S + 1);
+  int t;
+  if (u < hi) {
+    r.S = a.S + 1;
+    t = u / r.S;
+    r.split = u - t * r.S;
+    r.base = t * r.S;
+  } else {
+    r.S = a.S;
+    const int j = (u - hi) / a.S;
+    t = a.extra + j;
+    r.split = (u - hi) - j * a.S;
+    r.base = hi + j * a.S;
+  }
+  const int treg = a.p.batch * a.tps;
+  if (t < treg) {
+    r.seq = t / a.tps;
+    r.tile = t - r.seq * a.tps;
+  } else {
+    r.seq = 0;
+    r.tile = a.tps + (t - treg);
+  }
+  return r;
+}
+
+__device__ __forceinline__ int32_t list_entry(const AppendArgs& u, int e) {
+  return e < (int)u.a.len ? u.a.ptr[e] : u.b.ptr[e - (int)u.a.len];
+}
+
+// ------------------------------------------------------------------ fused step: the update's hand-off
+struct SplitPublish {
+  const SplitArgs* a;
+  uint32_t* words;  // shared: (tps + n_patch) * 4 drop words
+  int32_t* list;    // shared: the raw update lists (L entries)
+  __device__ void operator()(const StateView& sv, UpdSmem& sm, int n_old, int nl, int ne) const {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int nw = (a->tps + a->n_patch) * 4;
+    const int L = a->L;
+    for (int w = tid; w < nw; w += nt) words[w] = 0u;
+    for (int t = tid; t < L; t += nt) list[t] = list_entry(a->upd, t);
+    __syncthreads();
+    // pre-update slots whose id left I (the slot of every leaving id, hole[q])
+    for (int q = tid; q < nl; q += nt) atomicOr(&words[sm.hole[q] >> 5], 1u << (sm.hole[q] & 31));
+    // a patch row counts iff it is the first entry of its id, valid, on this
+    // shard, and its id enters I
+    for (int t = tid; t < L; t += nt) {
+      const int32_t g = list[t];
+      bool counts = g >= 0 && g < sv.vocab && is_local(sv, g);
+      for (int q = 0; counts && q < t; ++q) counts = list[q] != g;
+      if (counts) {
+        const int32_t lg = local_of(sv, g);
+        bool in = false;
+        for (int q = 0; q < ne && !in; ++q) in = sm.enter[q] == lg;
+        counts = in;
+      }
+      if (!counts) atomicOr(&words[a->tps * 4 + (t >> 5)], 1u << (t & 31));
+    }
+    __syncthreads();
+    for (int w = tid; w < nw; w += nt) a->drop[w] = words[w];
+    if (tid == 0) {
+      // every streaming CTA has read the pre-update slots / n_active: only
+      // then may ids[], pos[] and meta change (one-way wait: the streaming
+      // CTAs never wait, so they always get to arrive)
+      long long spins = 0;
+      while (ld_acquire(a->arrive_ctr) != (unsigned)a->heads)
+        if (++spins > kSpin) __trap();
+      *a->arrive_ctr = 0u;
+      __threadfence();
+    }
+    __syncthreads();
+  }
+};
+
+// ------------------------------------------------------------------ kernel A
+template <int NT, bool FUSED>
+__global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_constant__ SplitArgs a) {
+  using C = ACfg<NT>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStageArea);
+  // bars[0..St) full, [St..2St) empty, [2St] tmem_full, [2St+1] tmem_empty
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::kStages + 2);
+  __shared__ int32_t ids_s[2][kBM];  // the unit's row ids (double-buffered: the next unit's are prefetched)
+  __shared__ int sh_m[2];
+
+  const HeadProblem& p = a.p;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int KB = p.d / kBK;
+  if (tid == 0) trace_mark(p.trace, 0);
+  if (tid == 0 && p.trace) p.trace[(long long)blockIdx.x * kTraceSlots + 14] = clock64();
+  if (tid == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(smem_u32(&bars[s]), kLW);                // full: one arrival per loader warp
+      mbar_init(smem_u32(&bars[C::kStages + s]), 1);     // empty: one tcgen05.commit
+    }
+    mbar_init(smem_u32(&bars[2 * C::kStages]), 1);       // tmem_full
+    mbar_init(smem_u32(&bars[2 * C::kStages + 1]), kLW); // tmem_empty: one arrival per drain warp
+    fence_proxy_async();
+  }
+  if (warp == kLW) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(C::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // warm the translation and L2 line of the first unit's row ids (the first
+  // dependent round trip after the wait); the data itself is read after it
+  if ((int)blockIdx.x < a.units && tid < 4) {
+    const Unit u0 = unit_of(a, blockIdx.x);
+    if (u0.tile < a.tps) {
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(p.ids_base + (long long)u0.seq * p.ids_stride + u0.tile * kBM + 32 * tid));
+      if (tid == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.nact_base + (long long)u0.seq * p.nact_stride));
+    }
+  }
+  // everything above overlaps the previous kernel; its results (the state)
+  // are read only after this
+  pdl_wait();
+  // B (which waits for this grid to complete) may be scheduled now
+  asm volatile("griddepcontrol.launch_dependents;");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (tid == 0) trace_mark(p.trace, 1);
+
+  if (FUSED && (int)blockIdx.x == a.heads) {
+    // the updater: a2 while every other CTA streams
+    uint8_t* base = smem;
+    UpdSmem& us = *reinterpret_cast<UpdSmem*>(base);
+    uint32_t* words = reinterpret_cast<uint32_t*>(base + (sizeof(UpdSmem) + 255) / 256 * 256);
+    int32_t* list = reinterpret_cast<int32_t*>(words + (a.tps + a.n_patch) * 4);
+    SplitPublish pub{&a, words, list};
+    update_fast(a.upd, a.upd.seq0, us, pub, nullptr);
+    if (tid == 0) trace_mark(p.trace, 11);
+  } else {
+    constexpr uint32_t idesc = make_idesc(kBM, NT);
+    const int lr = tid >> 3;  // loader: 16-B chunk (tid & 7) of rows lr and lr + 64
+    const uint32_t swz = (uint32_t)(((tid & 7) ^ (lr & 7)) << 4);
+    int it = 0, local = 0, nrun = 0;  // pipeline iterations, units visited, units streamed
+    bool arrived = !FUSED;
+    const int stride = a.heads;
+    // ids of unit u into ids_s[buf]: one round trip (ids + n_active or the lists)
+    auto fetch_ids = [&](int u, int buf) {
+      const Unit un = unit_of(a, u);
+      if (un.tile < a.tps) {
+        const int row0 = un.tile * kBM;
+        if (tid < kBM)
+          ids_s[buf][tid] = row0 + tid < p.max_ids ? __ldcg(p.ids_base + (long long)un.seq * p.ids_stride + row0 + tid)
+                                                   : -1;
+        if (tid == kBM) sh_m[buf] = clamp_nact(p, un.seq) - row0;
+      } else {  // patch rows: the raw update-list entries (invalid / foreign ids are not streamed)
+        const int e = (un.tile - a.tps) * kBM + tid;
+        if (tid < kBM) {
+          int32_t g = e < a.L ? list_entry(a.upd, e) : -1;
+          if (!(g >= 0 && g < a.upd.sv.vocab && is_local(a.upd.sv, g))) g = -1;
+          ids_s[buf][tid] = g;
+        }
+        if (tid == kBM) sh_m[buf] = a.L - (un.tile - a.tps) * kBM;
+      }
+    };
+    if ((int)blockIdx.x < a.units) fetch_ids(blockIdx.x, 0);
+    __syncthreads();
+    if (tid == 0) trace_mark(p.trace, 7);
+    if (tid == 0 && p.trace) p.trace[(long long)blockIdx.x * kTraceSlots + 12] = clock64();
+    for (int u = blockIdx.x; u < a.units; u += stride, ++local) {
+      const int buf = local & 1;
+      const Unit un = unit_of(a, u);
+      const int rows = min(kBM, sh_m[buf]);  // rows of this tile in the row list (<= 0: none)
+      if (FUSED && !arrived && tid == kLoaders) {  // pre-update slots read (the MMA warp: no loader stalls)
+        red_add_release(a.arrive_ctr, 1u);
+        arrived = true;
+      }
+      // the tile's row ids for B (split 0 only); rows past the list: -1
+      if (un.split == 0 && un.tile == 0 && tid == kBM) a.mrows[un.seq] = sh_m[buf];
+      if (un.split == 0 && tid < kBM) {
+        const int32_t g = tid < rows ? ids_s[buf][tid] : -1;
+        a.rowgid[((long long)un.seq * (a.tps + a.n_patch) + un.tile) * kBM + tid] = g;
+      }
+      const int un_next = u + stride;
+      int32_t nx_id = -1;
+      int nx_m = 0;
+      bool nx = un_next < a.units;
+      if (nx) {  // prefetch the next unit's ids into registers (lands during the stream)
+        const Unit n2 = unit_of(a, un_next);
+        if (n2.tile < a.tps) {
+          const int row0 = n2.tile * kBM;
+          if (tid < kBM && row0 + tid < p.max_ids) nx_id = __ldcg(p.ids_base + (long long)n2.seq * p.ids_stride + row0 + tid);
+          if (tid == kBM) nx_m = clamp_nact(p, n2.seq) - row0;
+        }
+      }
+      if (rows <= 0) {
+        if (nx) {
+          if (tid < kBM) ids_s[buf ^ 1][tid] = nx_id;
+          if (tid == kBM) sh_m[buf ^ 1] = nx_m;
+        }
+        __syncthreads();
+        continue;
+      }
+      const int chunk = (un.split + un.tile) % un.S;  // rotated: the tiles read different H slices at once
+      const int kb0 = chunk * KB / un.S, kb1 = (chunk + 1) * KB / un.S;
+      const int nk = kb1 - kb0;
+      if (warp < kLW) {
+        // ---------------- loaders: rows of W_head + H into SW128 stages
+        const uint16_t* rp[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int r = lr + 64 * i;
+          const int32_t g = r < rows ? ids_s[buf][r] : -1;
+          const long long row = p.n_shards > 1 ? g / p.n_shards : g;
+          rp[i] = g >= 0 ? p.w + row * p.ldw + (tid & 7) * 8 : nullptr;
+        }
+        const uint16_t* hp = p.h + (long long)un.seq * p.n * p.d + (tid & 7) * 8;
+        uint64_t pol = 0;
+        if (a.w_evict_first) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        if (tid == 0 && local == 0) trace_mark(p.trace, 2);
+        if (tid == 0 && local == 0 && p.trace) p.trace[(long long)blockIdx.x * kTraceSlots + 13] = clock64();
+        for (int q = 0; q < nk + C::kStages - 1; ++q) {
+          if (q < nk) {
+            const int g_it = it + q;
+            const int stage = g_it % C::kStages;
+            if (g_it >= C::kStages) mbar_wait(smem_u32(&bars[C::kStages + stage]), ((g_it / C::kStages) - 1) & 1);
+            const uint32_t sA = smem_u32(smem + stage * C::kStageBytes);
+            const uint32_t sB = sA + C::kABytes;
+            const int kcol = (kb0 + q) * kBK;
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              if (a.w_evict_first)
+                cp_async16_hint(sA + (lr + 64 * i) * 128 + swz, rp[i] ? (const void*)(rp[i] + kcol) : (const void*)p.w,
+                                rp[i] ? 16u : 0u, pol);
+              else
+                cp_async16(sA + (lr + 64 * i) * 128 + swz, rp[i] ? (const void*)(rp[i] + kcol) : (const void*)p.w,
+                           rp[i] ? 16u : 0u);
+            }
+#pragma unroll
+            for (int i = 0; i < (NT * 8 + kLoaders - 1) / kLoaders; ++i) {
+              const int hr = lr + 64 * i;
+              if (hr < NT)
+                cp_async16(sB + hr * 128 + swz, hr < p.n ? (const void*)(hp + (long long)hr * p.d + kcol) : (const void*)p.h,
+                           hr < p.n ? 16u : 0u);
+            }
+          }
+          cp_async_commit();
+          if (q >= C::kStages - 1) {
+            cp_async_wait<C::kStages - 1>();
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&bars[(it + q - (C::kStages - 1)) % C::kStages]));
+          }
+        }
+        if (tid == 0 && local == 0) trace_mark(p.trace, 3);
+        // ---------------- drain: TMEM -> the unit's partial tile in L2
+        mbar_wait(smem_u32(&bars[2 * C::kStages]), nrun & 1);
+        tc_fence_after();
+        if (tid == 0 && nrun == 0) trace_mark(p.trace, 4);
+        const int lg = warp & 3, cgp = warp >> 2;
+        const int r = lg * 32 + lane;  // TMEM lane == tile row
+        const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16);
+        float* Pw = a.part + ((long long)(un.base + un.split) * p.n) * kBM + r;
+        if (cgp < C::kColGroups) {
+#pragma unroll 1
+          for (int c0 = cgp * 16; c0 < NT && c0 < p.n; c0 += 16 * C::kColGroups) {
+            float v[16];
+            tmem_ld16(taddr + c0, v);
+#pragma unroll
+            for (int c = 0; c < 16; ++c)
+              if (c0 + c < p.n) Pw[(c0 + c) * kBM] = v[c];
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&bars[2 * C::kStages + 1]));
+      } else {
+        // ---------------- MMA issue (warp 16, one lane)
+        if (nrun > 0) {  // the previous unit's partial has left TMEM
+          mbar_wait(smem_u32(&bars[2 * C::kStages + 1]), (nrun - 1) & 1);
+          tc_fence_after();
+        }
+        for (int q = 0; q < nk; ++q) {
+          const int g_it = it + q;
+          const int stage = g_it % C::kStages;
+          mbar_wait(smem_u32(&bars[stage]), (g_it / C::kStages) & 1);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t sA = smem_u32(smem + stage * C::kStageBytes);
+            const uint32_t sB = sA + C::kABytes;
+#pragma unroll
+            for (int kk = 0; kk < kBK / 16; ++kk)
+              umma_bf16(tmem, sw128_desc(sA + kk * 32), sw128_desc(sB + kk * 32), idesc, (q | kk) ? 1u : 0u);
+            umma_commit(smem_u32(&bars[C::kStages + stage]));
+            if (q == nk - 1) umma_commit(smem_u32(&bars[2 * C::kStages]));
+          }
+          __syncwarp();
+        }
+      }
+      it += nk;
+      ++nrun;
+      if (nx) {
+        if (tid < kBM) ids_s[buf ^ 1][tid] = nx_id;
+        if (tid == kBM) sh_m[buf ^ 1] = nx_m;
+      }
+      __syncthreads();  // ids_s[buf] free; the next unit's ids in ids_s[buf ^ 1]
+    }
+    if (FUSED && !arrived && tid == kLoaders) red_add_release(a.arrive_ctr, 1u);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kLW) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::kTmemCols));
+  }
+  if (tid == 0) trace_mark(p.trace, 9);
+  if (tid == 0 && p.trace) p.trace[(long long)blockIdx.x * kTraceSlots + 15] = clock64();
+}
+
+// ------------------------------------------------------------------ kernel B
+// One CTA (32 warps) per (sequence, node), in rounds of 32 tiles, one per warp
+// (the headline is one round).  Tiles are visited in the order [regular tiles
+// 0, tps) ++ [patch tiles]; a row counts iff its row id (written by A: -1 past
+// the row list) is >= 0 and its drop bit is clear, so no state is read: every
+// lane's loads -- the S partials of its 4 rows in K-chunk order, the row ids,
+// the drop bits -- are in flight at once (one round trip).  Per round: logits
+// and order keys; the threshold T = max(k-th key of the running top-k, the
+// 16-bit prefix of the round's k-th largest key) by a two-pass radix select
+// over shared-memory histograms (8 bits each: every thread adds its keys, one
+// warp finds the bin) -- at least k round keys are >= T, so no round key below
+// T is in the top-k; the few keys >= T (k plus the ties of a 16-bit prefix)
+// are appended behind the running top-k and every candidate is ranked by
+// counting by its own thread; lse = M + log sum exp(z - M) with M the block
+// maximum (one exp per row), folded across rounds.  No sequential merge of
+// lists anywhere.
+constexpr int kBThreads = 1024;
+constexpr int kBWarps = kBThreads / 32;
+constexpr int kRoundTiles = kBWarps;              // 32 tiles per round
+constexpr int kCand = kMaxK + kRoundTiles * kBM;  // worst case: every row of a round ties at T
+
+// One warp, a 256-bin histogram: the largest bin b whose suffix count
+// (bins >= b) reaches `need`, and how many keys are still needed inside it:
+// (b, need - count(bins > b)); (0xffffffff, need) when the total is below need.
+__device__ __forceinline__ uint2 radix_bin(const uint32_t* hist, uint32_t need) {
+  const int lane = threadIdx.x & 31;
+  uint32_t h[8], sum = 0u;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) { h[j] = hist[8 * lane + j]; sum += h[j]; }
+  uint32_t suf = sum;  // inclusive suffix over lanes >= this one
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_down_sync(0xffffffffu, suf, o);
+    if (lane + o < 32) suf += y;
+  }
+  const unsigned ok = __ballot_sync(0xffffffffu, suf >= need && need > 0u);
+  if (ok == 0u) return make_uint2(0xffffffffu, need);
+  const int L = 31 - __clz(ok);  // the highest lane whose suffix reaches need
+  const uint32_t above = __shfl_sync(0xffffffffu, suf - sum, L);  // keys in lanes > L
+  uint32_t bin = 0u, rem = 0u;
+  if (lane == L) {
+    uint32_t acc = above;
+#pragma unroll
+    for (int j = 7; j >= 0; --j) {
+      if (acc + h[j] >= need) { bin = 8u * lane + j; rem = need - acc; break; }
+      acc += h[j];
+    }
+  }
+  bin = __shfl_sync(0xffffffffu, bin, L);
+  rem = __shfl_sync(0xffffffffu, rem, L);
+  return make_uint2(bin, rem);
+}
+
+__global__ void __launch_bounds__(kBThreads, 1) head_select_kernel(const __grid_constant__ SplitArgs a) {
+  __shared__ uint2 cand[kCand];  // [0, k): the running top-k (sorted); then the round's candidates
+  __shared__ uint2 res[kMaxK];
+  __shared__ uint32_t hist1[256], hist2[256];
+  __shared__ uint32_t sh_wm[kBWarps];
+  __shared__ float sh_es[kBWarps];
+  __shared__ uint32_t sh_b1, sh_need, sh_T;
+  __shared__ int sh_cnt;
+  __shared__ float sh_M, sh_E;  // running lse: maximum and sum exp(z - maximum)
+  const HeadProblem& p = a.p;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int k = a.k;
+  const int seq = blockIdx.x / p.n, node = blockIdx.x - seq * p.n;
+  const int ntp = a.tps + a.n_patch;
+  const long long pst = (long long)p.n * kBM;
+  const int r0 = 4 * lane;
+  if (tid < kMaxK) cand[tid] = make_uint2(0u, 0xffffffffu);
+  if (tid < 256) { hist1[tid] = 0u; hist2[tid] = 0u; }
+  if (tid == 0) { sh_cnt = 0; sh_M = -INFINITY; sh_E = 0.f; }
+  if (tid == 0) trace_b(a, 0);
+  if (lane == 0 && warp < ntp) {  // warm the translations / L2 lines of round 0 while A still runs
+    int S0, b0;
+    tile_units(a, global_tile(a, seq, warp), S0, b0);
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.rowgid + ((long long)seq * ntp + warp) * kBM));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.part + (long long)b0 * pst + (long long)node * kBM));
+  }
+  pdl_wait();  // A complete: partials, row ids (and the fused step's drop bitmap) visible
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (tid == 0) trace_b(a, 1);
+  if (tid == 0 && p.trace) {
+    p.trace[(long long)(a.trace_base + blockIdx.x) * kTraceSlots + 14] = clock64();
+    p.trace[(long long)(a.trace_base + blockIdx.x) * kTraceSlots + 12] = 0xB;  // a B row
+  }
+  const int mrow = __ldcg(a.mrows + seq);  // regular tiles past it hold no rows (skipped after round 0)
+  for (int v0 = 0; v0 < ntp; v0 += kRoundTiles) {
+    const int treg = (mrow + kBM - 1) / kBM;
+    if (v0 > 0 && v0 >= treg && v0 + kRoundTiles <= a.tps) continue;  // a chunk of tiles past n_active
+    const int tile = v0 + warp;  // regular tiles [0, tps), then patch tiles
+    const bool on = tile < ntp && !(v0 > 0 && tile >= treg && tile < a.tps);
+    int S = 0, base = 0;
+    if (on) tile_units(a, global_tile(a, seq, tile), S, base);
+    const int4 g4 = on ? __ldcg(reinterpret_cast<const int4*>(a.rowgid + ((long long)seq * ntp + tile) * kBM) + lane)
+                       : make_int4(-1, -1, -1, -1);
+    const uint32_t dw = (on && a.drop) ? __ldcg(&a.drop[tile * 4 + (lane >> 3)]) >> ((lane & 7) * 4) : 0u;
+    float z[4] = {0.f, 0.f, 0.f, 0.f};
+    {
+      const float* src = a.part + (long long)base * pst + (long long)node * kBM + r0;
+      const int rot = S ? tile % S : 0;
+      for (int c0 = 0; c0 < S; c0 += 8) {  // K chunk c was computed by split (c - tile) mod S
+        float4 x[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (c0 + q < S) {
+            int sp = c0 + q - rot;
+            if (sp < 0) sp += S;
+            x[q] = __ldcg(reinterpret_cast<const float4*>(src + (long long)sp * pst));
+          }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (c0 + q < S) { z[0] += x[q].x; z[1] += x[q].y; z[2] += x[q].z; z[3] += x[q].w; }
+      }
+    }
+    if (tid == 0 && v0 == 0) trace_b(a, 5);
+    uint32_t key[4], gid[4];
+    uint32_t lm = 0u;
+    {
+      const int32_t g[4] = {g4.x, g4.y, g4.z, g4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const bool ok = g[i] >= 0 && !((dw >> i) & 1u);
+        key[i] = ok ? float_key(z[i]) : 0u;
+        gid[i] = ok ? (uint32_t)g[i] : 0xffffffffu;
+        lm = key[i] > lm ? key[i] : lm;
+        if (g[i] >= 0 && p.logits) {
+          const long long col = tile < a.tps ? (long long)tile * kBM + r0 + i
+                                             : (long long)p.max_ids + (tile - a.tps) * kBM + r0 + i;
+          p.logits[((long long)seq * p.n + node) * a.dbg_ld + col] = z[i];
+        }
+      }
+    }
+    // ---- pass 1 of the radix select: histogram of the keys' top 8 bits
+    const uint32_t wm = __reduce_max_sync(0xffffffffu, lm);
+    if (lane == 0) sh_wm[warp] = wm;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (key[i]) atomicAdd(&hist1[key[i] >> 24], 1u);
+    if (tid == 0 && v0 == 0) trace_b(a, 6);
+    __syncthreads();  // S1: histogram 1, warp maxima; the running top-k of the previous round
+    if (tid == 0 && v0 == 0) trace_b(a, 2);
+    const uint32_t Mk = __reduce_max_sync(0xffffffffu, sh_wm[lane]);  // the round's maximum key
+    const float M = key_value(Mk);
+    {  // lse partial of the round (one exp per row against the round maximum)
+      float es = 0.f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (key[i]) es += __expf(z[i] - M);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
+      if (lane == 0) sh_es[warp] = es;
+    }
+    if (warp == 0) {
+      const uint2 r = radix_bin(hist1, k);
+      if (lane == 0) { sh_b1 = r.x; sh_need = r.y; }
+    }
+    __syncthreads();  // S2: bin of the k-th largest key (top 8 bits), keys still needed inside it
+    const uint32_t b1 = sh_b1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (key[i] && (key[i] >> 24) == b1) atomicAdd(&hist2[(key[i] >> 16) & 0xffu], 1u);
+    __syncthreads();  // S3: histogram 2
+    if (warp == 0) {
+      // T = the 16-bit prefix of the round's k-th largest key (0: fewer than k
+      // keys); at least k round keys are >= T, so no round key below
+      // max(T, running k-th key) is in the top-k of (running list U round)
+      const uint2 r = radix_bin(hist2, sh_need);
+      const uint32_t T = b1 == 0xffffffffu ? 0u : (r.x == 0xffffffffu ? (b1 << 24) : (b1 << 24) | (r.x << 16));
+      const uint32_t Tk = cand[k - 1].x;
+      if (lane == 0) sh_T = T > Tk ? T : Tk;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) hist1[8 * lane + j] = 0u;  // ready for the next round
+    } else if (warp == kBWarps - 1) {  // fold the round's lse into the running one
+      float x = sh_es[lane];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane == 0 && Mk != 0u) lse_fold(sh_M, sh_E, M, x);
+    }
+    if (tid < k) res[tid] = make_uint2(0u, 0xffffffffu);  // fewer than k candidates: padding
+    __syncthreads();  // S4: threshold
+    const uint32_t T = sh_T;
+    // ---- the keys >= T go behind the running top-k
+    int c = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) c += (key[i] != 0u && key[i] >= T) ? 1 : 0;
+    if (__ballot_sync(0xffffffffu, c > 0)) {
+      int pre = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, pre, o);
+        if (lane >= o) pre += y;
+      }
+      int wbase = 0;
+      if (lane == 31) wbase = atomicAdd(&sh_cnt, pre);
+      wbase = __shfl_sync(0xffffffffu, wbase, 31);
+      int o2 = k + wbase + pre - c;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (key[i] != 0u && key[i] >= T) cand[o2++] = make_uint2(key[i], gid[i]);
+    }
+    __syncthreads();  // S5: candidates in place
+    if (tid == 0 && v0 == 0) trace_b(a, 7);
+    const int tot = k + sh_cnt;
+    for (int e = tid; e < tot; e += kBThreads) {  // every candidate ranked by its own thread
+      const uint2 me = cand[e];
+      if (me.x == 0u) continue;
+      int rk = 0;
+#pragma unroll 4
+      for (int f = 0; f < tot; ++f) {
+        const uint2 o = cand[f];
+        rk += (o.x != 0u && key_before(o.x, o.y, me.x, me.y)) ? 1 : 0;
+      }
+      if (rk < k) res[rk] = me;
+    }
+    if (tid < 256) hist2[tid] = 0u;
+    __syncthreads();  // S6: the round's top-k in res
+    if (tid == 0 && v0 == 0) trace_b(a, 9);
+    if (tid < k) cand[tid] = res[tid];  // the new running top-k
+    if (tid == 0) sh_cnt = 0;
+  }
+  if (warp != 0) return;
+  const long long ob = ((long long)seq * p.n + node) * k;
+  if (lane < k) {
+    const uint2 r = res[lane];
+    a.topk_logit[ob + lane] = r.x ? key_value(r.x) : -INFINITY;
+    a.topk_id[ob + lane] = r.x ? (int32_t)r.y : -1;
+  }
+  if (a.lse && lane == 0) a.lse[(long long)seq * p.n + node] = sh_M == -INFINITY ? -INFINITY : sh_M + logf(sh_E);
+  if (lane == 0) trace_b(a, 4);
+  if (lane == 0 && p.trace) p.trace[(long long)(a.trace_base + blockIdx.x) * kTraceSlots + 15] = clock64();
+}
+
+// ------------------------------------------------------------------ host side
+struct SplitLayout {
+  size_t part, rowgid, arrive, mrows, drop, total;
+};
+constexpr int kMaxPatch = kFastThreads / kBM;  // patch tiles (update lists <= kFastThreads entries)
+
+SplitLayout split_layout(int batch, int max_ids, int n, int num_sms) {
+  const size_t tps = (size_t)(max_ids + kBM - 1) / kBM;
+  const size_t tiles = (size_t)batch * tps + kMaxPatch;
+  const size_t units = tiles > (size_t)num_sms ? tiles : (size_t)num_sms;
+  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  SplitLayout L;
+  size_t off = 0;
+  L.part = off;   off += al(units * (size_t)n * kBM * sizeof(float));
+  L.rowgid = off; off += al(tiles * kBM * sizeof(int32_t));
+  L.arrive = off; off += al(sizeof(unsigned));
+  L.mrows = off;  off += al((size_t)batch * sizeof(int));
+  L.drop = off;   off += al((tps + kMaxPatch) * 4 * sizeof(uint32_t));
+  L.total = off;
+  return L;
+}
+
+int g_split_pdl = 1;
+// experiments (NANOSPEC_SPLIT_FLAGS): 1 = skip kernel B, 2 = no PDL, 4 = kernel B twice,
+// 8 = W rows with an L2 evict-first policy, 16 = kernel B alone
+int g_split_flags = -1;
+int split_flags() {
+  if (g_split_flags < 0) {
+    const char* e = getenv("NANOSPEC_SPLIT_FLAGS");
+    g_split_flags = e ? atoi(e) : 0;
+  }
+  return g_split_flags;
+}
+
+template <class K>
+cudaError_t launch_ex(K kern, dim3 grid, int threads, size_t smem, cudaStream_t stream, const SplitArgs& a,
+                      int cluster = 1) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (cluster > 1) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = cluster;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  const int base = na;
+  if (g_split_pdl && !(split_flags() & 2)) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
+  if (e != cudaSuccess && na > base) {  // without programmatic dependent launch
+    (void)cudaGetLastError();
+    cfg.numAttrs = base;
+    e = cudaLaunchKernelEx(&cfg, kern, a);
+  }
+  return e;
+}
+
+template <int NT, bool FUSED>
+cudaError_t set_attr_once() {
+  static bool done[64] = {false};  // per device: the attribute is per (function, device)
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (done[dev]) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(head_stream_kernel<NT, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       ACfg<NT>::kSmemBytes);
+  if (e == cudaSuccess) done[dev] = true;
+  return e;
+}
+
+template <int NT, bool FUSED>
+cudaError_t launch_pair_of_kernels(const SplitArgs& a, int grid_a, cudaStream_t stream) {
+  cudaError_t e = set_attr_once<NT, FUSED>();
+  if (e != cudaSuccess) return e;
+  SplitArgs b = a;
+  b.trace_base = grid_a;
+  if (!(split_flags() & 16)) {  // experiment 16: kernel B alone (on the previous call's partials)
+    e = launch_ex(head_stream_kernel<NT, FUSED>, dim3(grid_a), kAThreads, ACfg<NT>::kSmemBytes, stream, a);
+    if (e != cudaSuccess || (split_flags() & 1)) return e;
+  }
+  e = launch_ex(head_select_kernel, dim3(a.p.batch * a.p.n), kBThreads, 0, stream, b);
+  if (e != cudaSuccess || !(split_flags() & 4)) return e;
+  return launch_ex(head_select_kernel, dim3(a.p.batch * a.p.n), kBThreads, 0, stream, b);  // experiment
+}
+
+template <bool FUSED>
+cudaError_t launch_nt(const SplitArgs& a, int grid_a, cudaStream_t stream) {
+  const int n = a.p.n;
+  if (n <= 16) return launch_pair_of_kernels<16, FUSED>(a, grid_a, stream);
+  if (n <= 32) return launch_pair_of_kernels<32, FUSED>(a, grid_a, stream);
+  if (n <= 64) return launch_pair_of_kernels<64, FUSED>(a, grid_a, stream);
+  if (n <= 128) return launch_pair_of_kernels<128, FUSED>(a, grid_a, stream);
+  return launch_pair_of_kernels<256, FUSED>(a, grid_a, stream);
+}
+
+SplitArgs base_args(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse, void* scratch,
+                    const SplitLayout& L) {
+  SplitArgs a = {};
+  char* sc = (char*)scratch;
+  a.p = p;
+  a.part = (float*)(sc + L.part);
+  a.rowgid = (int32_t*)(sc + L.rowgid);
+  a.arrive_ctr = (unsigned*)(sc + L.arrive);
+  a.mrows = (int*)(sc + L.mrows);
+  a.drop = nullptr;
+  a.topk_logit = topk_logit;
+  a.topk_id = topk_id;
+  a.lse = lse;
+  a.k = k;
+  a.tps = (p.max_ids + kBM - 1) / kBM;
+  a.dbg_ld = p.max_ids;
+  a.w_evict_first = (split_flags() & 8) ? 1 : 0;
+  return a;
+}
+
+bool shape_ok(const HeadProblem& p, int k) {
+  return p.d % kBK == 0 && p.n >= 1 && p.n <= 256 && p.ldw % 8 == 0 && k >= 1 && k <= kMaxK && p.d / kBK >= 1;
+}
+
+}  // namespace
+
+size_t head_split_scratch_bytes(int batch, int max_ids, int n) { return split_layout(batch, max_ids, n, 256).total; }
+
+void set_head_split_pdl(int on) { g_split_pdl = on; }
+
+// Splits: U units on the SMs; every tile takes S = U / tiles K splits and the
+// first U % tiles tiles one more (S = 1 and a persistent loop when the tiles
+// outnumber the SMs).  A split holds at least one 64-column K atom.
+void plan_splits(SplitArgs& a, int U, int KB) {
+  const int nt = a.ntiles;
+  int S = nt <= U ? U / nt : 1;
+  int extra = nt <= U ? U - S * nt : 0;
+  if (S >= KB) { S = KB; extra = 0; }
+  if (S >= kMaxS) { S = kMaxS; extra = 0; }
+  a.S = S;
+  a.extra = extra;
+  a.units = nt * S + extra;
+}
+
+cudaError_t launch_head_split(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse,
+                             void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t stream) {
+  if (!shape_ok(p, k)) return cudaErrorNotSupported;
+  const int G = num_sms < 256 ? num_sms : 256;
+  const SplitLayout L = split_layout(p.batch, p.max_ids, p.n, 256);
+  if (L.total > scratch_bytes) return cudaErrorInvalidValue;
+  SplitArgs a = base_args(p, k, topk_logit, topk_id, lse, scratch, L);
+  a.n_patch = 0;
+  a.ntiles = p.batch * a.tps;
+  plan_splits(a, G, p.d / kBK);
+  a.heads = a.units < G ? a.units : G;
+  return launch_nt<false>(a, a.heads, stream);
+}
+
+cudaError_t launch_step_split(const HeadProblem& p, const AppendArgs& upd, int k, float* topk_logit,
+                              int32_t* topk_id, float* lse, void* scratch, size_t scratch_bytes, int num_sms,
+                              cudaStream_t stream, bool dry_run) {
+  if (!shape_ok(p, k) || p.batch != 1) return cudaErrorNotSupported;
+  const long long Lr = upd.a.len + upd.b.len;
+  const int G = num_sms < 256 ? num_sms : 256;
+  const int tps = (p.max_ids + kBM - 1) / kBM;
+  const int n_patch = Lr <= 0 ? 0 : (int)((Lr + kBM - 1) / kBM);
+  // one wave: every streaming CTA plus the updater resident at once is not
+  // required (nobody waits for a streaming CTA), but each tile needs a CTA
+  if (n_patch > kMaxPatch || tps + n_patch + 1 > G) return cudaErrorNotSupported;
+  // the updater's shared memory: UpdSmem + drop words + the raw lists
+  if ((sizeof(UpdSmem) + 255) / 256 * 256 + (size_t)(tps + n_patch) * 16 + (size_t)Lr * 4 > (size_t)kBudget)
+    return cudaErrorNotSupported;
+  if (dry_run) return cudaSuccess;
+  const SplitLayout L = split_layout(1, p.max_ids, p.n, 256);
+  if (L.total > scratch_bytes) return cudaErrorInvalidValue;
+  SplitArgs a = base_args(p, k, topk_logit, topk_id, lse, scratch, L);
+  a.n_patch = n_patch;
+  a.ntiles = tps + n_patch;
+  plan_splits(a, G - 1, p.d / kBK);
+  a.heads = a.units;
+  a.upd = upd;
+  a.L = (int)Lr;
+  a.drop = (uint32_t*)((char*)scratch + L.drop);
+  a.dbg_ld = (long long)p.max_ids + Lr;
+  return launch_nt<true>(a, a.heads + 1, stream);
+}
+
+}  // namespace nanospec

@@ -77,6 +77,7 @@ constexpr int kModePoll = 1;     // one unit per CTA, split-K partials + lists h
 constexpr int kModeCluster = 2;  // one unit per CTA, the S splits of a tile form a cluster (DSMEM reduction)
 constexpr int kModeFused = 3;    // cluster mode + the state update in the same launch (patch tiles)
 constexpr int kModePair = 6;     // opt-in: the pair-split kernel of head_pair.cu
+constexpr int kModeSplit = 7;    // the two-kernel head of head_split.cu (also what auto takes first)
 constexpr int kMaxCluster = 8;   // portable cluster size
 constexpr int kMaxL2Lists = 160;  // poll mode: tiles per sequence (5 lists per lane at level 2)
 constexpr long long kSpinLimit = 1ll << 26;  // polls before giving up (a trap beats a hung GPU)
@@ -1387,7 +1388,10 @@ cudaError_t launch_step_nt(const HeadProblem& p, const AppendArgs& upd, int k, f
 
 }  // namespace
 
-size_t head_tc_scratch_bytes(int batch, int max_ids, int n) { return scratch_layout(batch, max_ids, n).total; }
+// The split head's scratch follows the older kernels' (whose counters must stay zero between launches).
+size_t head_tc_scratch_bytes(int batch, int max_ids, int n) {
+  return scratch_layout(batch, max_ids, n).total + head_split_scratch_bytes(batch, max_ids, n);
+}
 
 void set_head_tc_mode(int mode) { g_head_mode = mode; }
 void set_head_tc_cluster_cap(int s) { g_cluster_cap = s; }
@@ -1409,6 +1413,12 @@ PairScratch pair_scratch(void* scratch, const ScratchLayout& L) {
 cudaError_t launch_step_tc(const HeadProblem& p, const AppendArgs& upd, int k, float* topk_logit, int32_t* topk_id,
                            float* lse, void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t stream,
                            bool dry_run) {
+  if (g_head_mode == -1 || g_head_mode == kModeSplit) {  // default: the two-kernel head (head_split.cu)
+    const size_t off = scratch_layout(1, p.max_ids, p.n).total;
+    const cudaError_t e = launch_step_split(p, upd, k, topk_logit, topk_id, lse, dry_run ? nullptr : (char*)scratch + off,
+                                            dry_run ? 0 : scratch_bytes - off, num_sms, stream, dry_run);
+    if (e != cudaErrorNotSupported || g_head_mode == kModeSplit) return e;
+  }
   if (g_head_mode == kModePair) {  // opt-in: the pair-split kernel (head_pair.cu)
     const ScratchLayout L = scratch_layout(1, p.max_ids, p.n);
     if (dry_run || L.total <= scratch_bytes) {
@@ -1430,8 +1440,24 @@ cudaError_t launch_step_tc(const HeadProblem& p, const AppendArgs& upd, int k, f
 #undef NS_STEP
 }
 
+cudaError_t launch_step_split_only(const HeadProblem& p, const AppendArgs& upd, int k, float* topk_logit,
+                                   int32_t* topk_id, float* lse, void* scratch, size_t scratch_bytes, int num_sms,
+                                   cudaStream_t stream) {
+  const size_t off = scratch_layout(1, p.max_ids, p.n).total;
+  if (off > scratch_bytes) return cudaErrorInvalidValue;
+  return launch_step_split(p, upd, k, topk_logit, topk_id, lse, (char*)scratch + off, scratch_bytes - off, num_sms,
+                           stream, false);
+}
+
 cudaError_t launch_head_tc(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse,
                            void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t stream) {
+  if (g_head_mode == -1 || g_head_mode == kModeSplit) {  // default: the two-kernel head (head_split.cu)
+    const size_t off = scratch_layout(p.batch, p.max_ids, p.n).total;
+    if (off > scratch_bytes) return cudaErrorInvalidValue;
+    const cudaError_t e = launch_head_split(p, k, topk_logit, topk_id, lse, (char*)scratch + off, scratch_bytes - off,
+                                            num_sms, stream);
+    if (e != cudaErrorNotSupported || g_head_mode == kModeSplit) return e;
+  }
   if (g_head_mode == kModePair) {  // opt-in: the pair-split kernel (head_pair.cu)
     const ScratchLayout L = scratch_layout(p.batch, p.max_ids, p.n);
     if (L.total > scratch_bytes) return cudaErrorInvalidValue;

@@ -70,6 +70,20 @@ cudaError_t launch_step_pair(const HeadProblem& p, const AppendArgs& upd, int k,
                              int32_t* topk_id, float* lse, const PairScratch& s, int num_sms, cudaStream_t stream,
                              bool dry_run);
 void set_head_pair_enabled(int on);
+// Two-kernel head (head_split.cu): stream kernel A (gather + UMMA + partials to
+// L2) and select kernel B (sum + top-k + lse), chained by programmatic
+// dependent launch.  Scratch: head_split_scratch_bytes at the start of `scratch`.
+size_t head_split_scratch_bytes(int batch, int max_ids, int n);
+cudaError_t launch_head_split(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse,
+                              void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t stream);
+cudaError_t launch_step_split(const HeadProblem& p, const AppendArgs& upd, int k, float* topk_logit,
+                              int32_t* topk_id, float* lse, void* scratch, size_t scratch_bytes, int num_sms,
+                              cudaStream_t stream, bool dry_run);
+void set_head_split_pdl(int on);
+// The fused step through the split head only (the debug-logits call); scratch as launch_step_tc.
+cudaError_t launch_step_split_only(const HeadProblem& p, const AppendArgs& upd, int k, float* topk_logit,
+                                   int32_t* topk_id, float* lse, void* scratch, size_t scratch_bytes, int num_sms,
+                                   cudaStream_t stream);
 // Whether launch_state_append would take the per-step fast path for these lists.
 bool state_fast_path(const StateView& sv, int reset, long long a_len, int a_dedup, long long b_len, int b_dedup);
 // Debug: force the fused head's reduction mode (-1 auto, 0 finisher, 1 poll, 2 cluster).

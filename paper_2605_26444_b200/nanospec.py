@@ -160,6 +160,16 @@ class HeadOutputs:
         self.scratch = torch.zeros(nbytes, dtype=torch.uint8, device=device)
 
 
+def _check_out(out: HeadOutputs, batch: int, n_nodes: int, k: int, max_ids: int, debug: bool = False):
+    """A caller-supplied HeadOutputs must match the call: the kernels write
+    [batch, n_nodes, k] outputs and use a scratch sized for max_ids rows."""
+    if out.batch != batch or out.n_nodes != n_nodes or out.k != k or out.max_ids < max_ids:
+        raise ValueError(f"HeadOutputs(batch={out.batch}, n_nodes={out.n_nodes}, k={out.k}, max_ids={out.max_ids}) "
+                         f"does not fit a call with batch={batch}, n_nodes={n_nodes}, k={k}, max_ids={max_ids}")
+    if debug and out.debug_logits is None:
+        raise ValueError("debug logits requested but the HeadOutputs has no debug buffer")
+
+
 def draft_logits_topk(state: ActiveVocab, w_head: torch.Tensor, hidden: torch.Tensor, k: int, *,
                       lse: bool = True, debug_logits: bool = False, impl: str = "auto",
                       out: HeadOutputs | None = None):
@@ -176,6 +186,7 @@ def draft_logits_topk(state: ActiveVocab, w_head: torch.Tensor, hidden: torch.Te
         raise ValueError("hidden must be [batch, n_nodes, d] with the weight's d")
     if out is None:
         out = HeadOutputs(state.batch, n_nodes, k, state.w_max, hidden.device, lse, debug_logits)
+    _check_out(out, state.batch, n_nodes, k, state.w_max, debug_logits)
     st = N.lib().nanospec_draft_logits_topk_ex(
         state.handle, _ptr(w_head), d, w_head.stride(0), _ptr(hidden), n_nodes, k, _ptr(out.topk_logit),
         _ptr(out.topk_id), _ptr(out.lse), _ptr(out.debug_logits), _ptr(out.scratch), out.scratch.numel(),
@@ -199,6 +210,7 @@ def step(state: ActiveVocab, seq: int, draft: torch.Tensor | None, verify: torch
             _need(t, torch.int32, name)
     if out is None:
         out = HeadOutputs(1, n_nodes, k, state.w_max, hidden.device, lse, False)
+    _check_out(out, 1, n_nodes, k, state.w_max)
     st = N.lib().nanospec_step(
         state.handle, seq, _ptr(draft), 0 if draft is None else draft.numel(), _ptr(verify),
         0 if verify is None else verify.numel(), _ptr(w_head), d, w_head.stride(0), _ptr(hidden), n_nodes, k,
@@ -206,6 +218,30 @@ def step(state: ActiveVocab, seq: int, draft: torch.Tensor | None, verify: torch
         _stream(hidden.device))
     N.check(st, "nanospec_step")
     return out.topk_logit, out.topk_id, out.lse
+
+
+def step_debug(state: ActiveVocab, seq: int, draft: torch.Tensor | None, verify: torch.Tensor | None,
+               w_head: torch.Tensor, hidden: torch.Tensor, k: int, *, out: HeadOutputs | None = None):
+    """step() in its fused launch, also returning the logits of every streamed
+    row: [n_nodes, w_max + n_draft + k_ver] -- the pre-update slots, then the
+    update-list entries (nanospec_step_debug).  Raises EUNSUPPORTED when the
+    step cannot be fused."""
+    _need(w_head, torch.bfloat16, "w_head")
+    _need(hidden, torch.bfloat16, "hidden")
+    d = w_head.shape[-1]
+    n_nodes = hidden.numel() // d
+    nd = 0 if draft is None else _need(draft, torch.int32, "draft").numel()
+    kv = 0 if verify is None else _need(verify, torch.int32, "verify").numel()
+    if out is None:
+        out = HeadOutputs(1, n_nodes, k, state.w_max, hidden.device)
+    _check_out(out, 1, n_nodes, k, state.w_max)
+    dbg = torch.full((n_nodes, state.w_max + nd + kv), float("nan"), dtype=torch.float32, device=hidden.device)
+    st = N.lib().nanospec_step_debug(
+        state.handle, seq, _ptr(draft), nd, _ptr(verify), kv, _ptr(w_head), d, w_head.stride(0), _ptr(hidden), n_nodes,
+        k, _ptr(out.topk_logit), _ptr(out.topk_id), _ptr(out.lse), _ptr(dbg), _ptr(out.scratch), out.scratch.numel(),
+        _stream(hidden.device))
+    N.check(st, "nanospec_step_debug")
+    return out.topk_logit, out.topk_id, out.lse, dbg
 
 
 class StepHostIO:
@@ -225,9 +261,17 @@ class StepHostIO:
         self.d_io = torch.empty(total, dtype=torch.uint8, device=device)
         self.scratch = HeadOutputs(1, n_nodes, k, w_max, device).scratch
         self.h_out = torch.empty(self.out_bytes, dtype=torch.uint8).pin_memory()
+        # input blocks handed to nanospec_step_host stay referenced until the
+        # stream has consumed them (the library's cudaMemcpyAsync is invisible
+        # to torch's pinned-memory allocator, which could otherwise recycle them)
+        self._inflight = []
+
+    def _retire(self):
+        self._inflight = [(ev, blk) for ev, blk in self._inflight if not ev.query()]
 
     def pack_inputs(self, hidden: torch.Tensor, draft, verify) -> torch.Tensor:
         """A pinned host block holding one step's inputs."""
+        self._retire()
         blk = torch.zeros(self.in_bytes, dtype=torch.uint8).pin_memory()
         hb = self.n * self.d * 2
         blk[:hb].view(torch.bfloat16).copy_(hidden.reshape(-1).cpu())
@@ -253,6 +297,9 @@ def step_host(state: ActiveVocab, seq: int, io: StepHostIO, h_in: torch.Tensor, 
         io.h_out.data_ptr(), _ptr(io.d_io), io.d_io.numel(), _ptr(io.scratch), io.scratch.numel(),
         _stream(w_head.device))
     N.check(st, "nanospec_step_host")
+    ev = torch.cuda.Event()
+    ev.record(torch.cuda.current_stream(w_head.device))
+    io._inflight.append((ev, h_in))
 
 
 def step_is_fused(state: ActiveVocab, n_draft: int, k_ver: int, d_model: int, n_nodes: int, k: int) -> bool:
@@ -273,6 +320,7 @@ def logits_topk_ids(ids: torch.Tensor, n_ids: torch.Tensor, w_head: torch.Tensor
     n_nodes = hidden.numel() // d
     if out is None:
         out = HeadOutputs(1, n_nodes, k, ids.numel(), hidden.device, lse, debug_logits)
+    _check_out(out, 1, n_nodes, k, ids.numel(), debug_logits)
     st = N.lib().nanospec_logits_topk_ids(
         _ptr(ids), _ptr(n_ids), ids.numel(), n_shards, _ptr(w_head), d, w_head.stride(0), _ptr(hidden), n_nodes, k,
         _ptr(out.topk_logit), _ptr(out.topk_id), _ptr(out.lse), _ptr(out.debug_logits), _ptr(out.scratch),
