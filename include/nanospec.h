@@ -210,15 +210,18 @@ nanospec_status nanospec_merge_topk(const float* d_cand_logit, const int32_t* d_
                                     int32_t n_shards, int32_t n_rows, int32_t k, float* d_out_logit,
                                     int32_t* d_out_id, float* d_out_lse, cudaStream_t stream);
 
-/* One decode step of sequence `seq` in ONE launch where possible: the state
- * update (Eq. 4 + Eq. 5; exactly nanospec_state_update) followed by
- * the restricted head over the UPDATED active set (Eq. 2 on I, P:205;
+/* One decode step of sequence `seq`, fused where possible: the state update
+ * (Eq. 4 + Eq. 5; exactly nanospec_state_update) followed by the
+ * restricted head over the UPDATED active set (Eq. 2 on I, P:205;
  * SelectDraftTokens P:527-528; exactly nanospec_draft_logits_topk on that
- * sequence).  The fused kernel streams the rows of the pre-update slots while
- * one CTA applies the update, then adds the entering ids as patch tiles and
- * drops the rows whose id left I, so the update is off the critical path.
- * Shapes it cannot fuse (rule R2, lists > 512 ids, large windows, clusters
- * that do not fit one wave) run as two launches with identical results.
+ * sequence).  Fused, the head's stream kernel gathers the rows of the
+ * pre-update slots plus the update-list entries (a superset of the new I
+ * known without waiting for the update) while one of its CTAs applies the
+ * update, and the select kernel drops the rows that are not in the new I, so
+ * the update is off the critical path (two kernels, no CTA waits for another
+ * except the updating CTA for the streaming ones).  Shapes it cannot fuse
+ * (rule R2, lists > 512 ids, more row tiles than SMs) run as update + head
+ * with identical results.
  *   d_draft_ids int32[n_draft], d_verify_topk int32[k_ver]  (as state_update)
  *   d_hidden    bf16 [n_nodes x d_model] (this sequence's tree nodes)
  *   d_topk_logit / d_topk_id [n_nodes x k], d_lse [n_nodes] or NULL
@@ -238,7 +241,7 @@ nanospec_status nanospec_step(nanospec_state st, int32_t seq, const int32_t* d_d
  *     columns [w_max, w_max + e)  the update-list entries, draft then verify.
  *   Only the rows in the updated active set feed the top-k / lse (the others
  *   are rows whose id left I, repeats, or ids that were already active).
- * EUNSUPPORTED when the step cannot run as one fused launch (then nothing is
+ * EUNSUPPORTED when the step cannot run fused (then nothing is
  * done); otherwise exactly nanospec_step. */
 nanospec_status nanospec_step_debug(nanospec_state st, int32_t seq, const int32_t* d_draft_ids, int32_t n_draft,
                                     const int32_t* d_verify_topk, int32_t k_ver, const void* d_w_head,
@@ -260,30 +263,30 @@ nanospec_status nanospec_step_host(nanospec_state st, int32_t seq, const void* h
                                    void* h_out, void* d_io, size_t io_bytes, void* d_scratch, size_t scratch_bytes,
                                    cudaStream_t stream);
 
-/* 1 if nanospec_step with these sizes runs as ONE fused launch on the current
- * device, 0 if it runs as update + head (same results).  Host-only query. */
+/* 1 if nanospec_step with these sizes runs fused (the update inside the head's
+ * stream kernel) on the current device, 0 if it runs as update + head (same
+ * results).  Host-only query. */
 int32_t nanospec_step_fused(const nanospec_state st, int32_t n_draft, int32_t k_ver, int32_t d_model,
                             int32_t n_nodes, int32_t k);
 
-/* Debug: phase trace.  d_buf = device uint64[ctas * 16] (ctas >= 256) or NULL
- * (off, the default).  While set, the fused tensor-core head writes the
- * %globaltimer (ns) of its phases, CTA b at d_buf[b*16 + e]: 0 start,
- * 1 dependency resolved, 2 row pointers ready, 3 last load landed, 4 last MMA
- * done, 5 reduction inputs visible, 7 ids staged, 8 done, 9 drained,
- * 10-13 tail phases (scripts/trace_head.py names them), 14/15 clock64 at
- * start / end.  Process-wide; not thread-safe; for profiling only. */
+/* Debug: phase trace.  d_buf = device uint64[ctas * 16] (ctas >= 256; rows for
+ * the stream kernel's grid plus the select kernel's) or NULL (off, the
+ * default).  While set, the tensor-core head writes %globaltimer (ns) marks:
+ * stream-kernel CTA b at d_buf[b*16 + e] (0 start, 1 dependency resolved, 7
+ * row ids staged, 2 first loads, 3 last load landed, 4 last MMA done, 9
+ * drained, 11 update published; 12/13/14/15 clock64), select-kernel CTA c at
+ * row (stream grid + c) (0 start, 1 dependency resolved, 5 partials loaded,
+ * 6/2 histogram, 7 candidates, 9 ranked, 4 done; 12 = 0xB marks the row;
+ * scripts/split_dev.py prints them).  Process-wide; not thread-safe; for
+ * profiling only. */
 nanospec_status nanospec_debug_set_trace(unsigned long long* d_buf, int32_t ctas);
 
-/* Debug: force the fused tensor-core head's split-K reduction mode for the
- * following calls: -1 automatic (default), 0 persistent CTAs + grid barrier +
- * one finisher CTA per (sequence, node), 1 one unit per CTA with L2 hand-off
- * (poll), 2 clusters of K-split CTAs with DSMEM reduction.  A forced mode the
- * shape cannot use falls back to the automatic choice.  Process-wide; tests. */
+/* Debug: -1 (default) launches the tensor-core head's two kernels (stream
+ * kernel A, select kernel B) with programmatic dependent launch, so each one's
+ * prologue overlaps its predecessor; 0 launches them in plain stream order
+ * (same results); 1 launches the stream kernel alone (timing breakdowns only:
+ * no outputs are written).  Process-wide; tests and bench. */
 nanospec_status nanospec_debug_set_head_mode(int32_t mode);
-
-/* Debug: cap the thread-block-cluster size (K splits per row tile, 2..8) the
- * cluster-mode head and the fused step try; 0 = no cap (default).  Tests. */
-nanospec_status nanospec_debug_set_cluster_cap(int32_t s);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -23,7 +23,7 @@ EXPORTS = [
     "nanospec_head_scratch_bytes", "nanospec_draft_logits_topk", "nanospec_draft_logits_topk_ex",
     "nanospec_logits_topk_ids", "nanospec_merge_topk", "nanospec_debug_set_trace",
     "nanospec_debug_set_head_mode", "nanospec_step", "nanospec_step_fused", "nanospec_step_debug",
-    "nanospec_debug_set_cluster_cap", "nanospec_step_host", "nanospec_step_host_io_bytes",
+    "nanospec_step_host", "nanospec_step_host_io_bytes",
 ]
 
 
@@ -71,7 +71,6 @@ def lib():
     L.nanospec_merge_topk.argtypes = [vp, vp, vp, i32, i32, i32, vp, vp, vp, vp]
     L.nanospec_debug_set_trace.argtypes = [vp, i32]
     L.nanospec_debug_set_head_mode.argtypes = [i32]
-    L.nanospec_debug_set_cluster_cap.argtypes = [i32]
     L.nanospec_step_host_io_bytes.argtypes = [i32, i32, i32, i32, i32, ctypes.POINTER(sz), ctypes.POINTER(sz)]
     L.nanospec_step_host_io_bytes.restype = sz
     L.nanospec_step_host.argtypes = [vp, i32, vp, i32, i32, vp, i32, i64, i32, i32, vp, vp, sz, vp, sz, vp]

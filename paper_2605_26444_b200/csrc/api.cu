@@ -328,11 +328,8 @@ nanospec_status step_impl(nanospec_state st, int32_t seq, const int32_t* d_draft
     upd.a = ListArg{d_draft_ids, d_draft_ids ? n_draft : 0, 0, 1};
     upd.b = ListArg{d_verify_topk, d_verify_topk ? k_ver : 0, 0, 1};
     const size_t lb = logits_bytes(1, sv.w_max, n_nodes);
-    cudaError_t e = d_debug_logits
-                        ? launch_step_split_only(hp, upd, k, d_topk_logit, d_topk_id, d_lse, (char*)d_scratch + lb,
-                                                 scratch_bytes - lb, sm_count(), stream)
-                        : launch_step_tc(hp, upd, k, d_topk_logit, d_topk_id, d_lse, (char*)d_scratch + lb,
-                                         scratch_bytes - lb, sm_count(), stream);
+    cudaError_t e = launch_step_tc(hp, upd, k, d_topk_logit, d_topk_id, d_lse, (char*)d_scratch + lb,
+                                   scratch_bytes - lb, sm_count(), stream);
     if (e == cudaSuccess) return NANOSPEC_OK;
     if (e != cudaErrorNotSupported) return NANOSPEC_ECUDA;
   }
@@ -455,14 +452,8 @@ nanospec_status nanospec_debug_set_trace(unsigned long long* d_buf, int32_t ctas
 }
 
 nanospec_status nanospec_debug_set_head_mode(int32_t mode) {
-  if (mode < -1 || mode > 7 || mode == 5) return NANOSPEC_EINVAL;
+  if (mode < -1 || mode > 1) return NANOSPEC_EINVAL;
   set_head_tc_mode(mode);
-  return NANOSPEC_OK;
-}
-
-nanospec_status nanospec_debug_set_cluster_cap(int32_t s) {
-  if (s < 0 || s > 8) return NANOSPEC_EINVAL;
-  set_head_tc_cluster_cap(s % 16);
   return NANOSPEC_OK;
 }
 

@@ -98,6 +98,19 @@ struct SplitArgs {
   int w_evict_first;    // W rows streamed with an L2 evict-first policy
 };
 
+// The kernel parameters live in the constant bank; their first reads miss the
+// constant cache (an L2 round trip each, and the index math chains several).
+// Touch every 64-byte line of the parameter block before waiting on the
+// previous grid, so those misses overlap the wait.
+__device__ __forceinline__ void warm_params(const SplitArgs& a) {
+  constexpr int kLines = (int)((sizeof(SplitArgs) + 63) / 64);
+  const int t = threadIdx.x;
+  if (t < kLines) {
+    const int v = reinterpret_cast<const int*>(&a)[t * 16];
+    asm volatile("" ::"r"(v));
+  }
+}
+
 __device__ __forceinline__ void trace_b(const SplitArgs& a, int e) {
   if (a.p.trace) a.p.trace[(long long)(a.trace_base + blockIdx.x) * kTraceSlots + e] = globaltimer();
 }
@@ -138,6 +151,22 @@ __device__ __forceinline__ Unit unit_of(const SplitArgs& a, int u) {
     r.seq = 0;
     r.tile = a.tps + (t - treg);
   }
+  return r;
+}
+
+// A unit with its K range: chunk (split + tile) mod S of the tile's K atoms
+// (rotated, so the tiles read different slices of H at any moment).
+struct UnitPlan {
+  int seq, tile, split, S, base, kb0, nk;
+};
+__device__ __forceinline__ UnitPlan plan_unit(const SplitArgs& a, int u) {
+  const Unit un = unit_of(a, u);
+  UnitPlan r;
+  r.seq = un.seq; r.tile = un.tile; r.split = un.split; r.S = un.S; r.base = un.base;
+  const int KB = a.p.d / kBK;
+  const int chunk = (un.split + un.tile) % un.S;
+  r.kb0 = chunk * KB / un.S;
+  r.nk = (chunk + 1) * KB / un.S - r.kb0;
   return r;
 }
 
@@ -220,14 +249,14 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
                  "n"(C::kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  // warm the translation and L2 line of the first unit's row ids (the first
-  // dependent round trip after the wait); the data itself is read after it
-  if ((int)blockIdx.x < a.units && tid < 4) {
-    const Unit u0 = unit_of(a, blockIdx.x);
-    if (u0.tile < a.tps) {
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(p.ids_base + (long long)u0.seq * p.ids_stride + u0.tile * kBM + 32 * tid));
-      if (tid == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.nact_base + (long long)u0.seq * p.nact_stride));
-    }
+  warm_params(a);
+  // the first unit's plan (index math only) and a warm-up of the translation
+  // and L2 line of its row ids (the first dependent round trip after the
+  // wait); the state itself is read only after the wait
+  UnitPlan cur = plan_unit(a, (int)blockIdx.x < a.units ? (int)blockIdx.x : 0);
+  if ((int)blockIdx.x < a.units && tid < 4 && cur.tile < a.tps) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p.ids_base + (long long)cur.seq * p.ids_stride + cur.tile * kBM + 32 * tid));
+    if (tid == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.nact_base + (long long)cur.seq * p.nact_stride));
   }
   // everything above overlaps the previous kernel; its results (the state)
   // are read only after this
@@ -257,8 +286,7 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
     bool arrived = !FUSED;
     const int stride = a.heads;
     // ids of unit u into ids_s[buf]: one round trip (ids + n_active or the lists)
-    auto fetch_ids = [&](int u, int buf) {
-      const Unit un = unit_of(a, u);
+    auto fetch_ids = [&](const UnitPlan& un, int buf) {
       if (un.tile < a.tps) {
         const int row0 = un.tile * kBM;
         if (tid < kBM)
@@ -275,13 +303,13 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
         if (tid == kBM) sh_m[buf] = a.L - (un.tile - a.tps) * kBM;
       }
     };
-    if ((int)blockIdx.x < a.units) fetch_ids(blockIdx.x, 0);
+    if ((int)blockIdx.x < a.units) fetch_ids(cur, 0);
     __syncthreads();
     if (tid == 0) trace_mark(p.trace, 7);
     if (tid == 0 && p.trace) p.trace[(long long)blockIdx.x * kTraceSlots + 12] = clock64();
     for (int u = blockIdx.x; u < a.units; u += stride, ++local) {
       const int buf = local & 1;
-      const Unit un = unit_of(a, u);
+      const UnitPlan un = cur;
       const int rows = min(kBM, sh_m[buf]);  // rows of this tile in the row list (<= 0: none)
       if (FUSED && !arrived && tid == kLoaders) {  // pre-update slots read (the MMA warp: no loader stalls)
         red_add_release(a.arrive_ctr, 1u);
@@ -298,7 +326,8 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
       int nx_m = 0;
       bool nx = un_next < a.units;
       if (nx) {  // prefetch the next unit's ids into registers (lands during the stream)
-        const Unit n2 = unit_of(a, un_next);
+        const UnitPlan n2 = plan_unit(a, un_next);
+        cur = n2;
         if (n2.tile < a.tps) {
           const int row0 = n2.tile * kBM;
           if (tid < kBM && row0 + tid < p.max_ids) nx_id = __ldcg(p.ids_base + (long long)n2.seq * p.ids_stride + row0 + tid);
@@ -313,9 +342,7 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
         __syncthreads();
         continue;
       }
-      const int chunk = (un.split + un.tile) % un.S;  // rotated: the tiles read different H slices at once
-      const int kb0 = chunk * KB / un.S, kb1 = (chunk + 1) * KB / un.S;
-      const int nk = kb1 - kb0;
+      const int kb0 = un.kb0, nk = un.nk;
       if (warp < kLW) {
         // ---------------- loaders: rows of W_head + H into SW128 stages
         const uint16_t* rp[2];
@@ -498,6 +525,7 @@ __global__ void __launch_bounds__(kBThreads, 1) head_select_kernel(const __grid_
   const int ntp = a.tps + a.n_patch;
   const long long pst = (long long)p.n * kBM;
   const int r0 = 4 * lane;
+  warm_params(a);
   if (tid < kMaxK) cand[tid] = make_uint2(0u, 0xffffffffu);
   if (tid < 256) { hist1[tid] = 0u; hist2[tid] = 0u; }
   if (tid == 0) { sh_cnt = 0; sh_M = -INFINITY; sh_E = 0.f; }
@@ -508,6 +536,10 @@ __global__ void __launch_bounds__(kBThreads, 1) head_select_kernel(const __grid_
     asm volatile("prefetch.global.L2 [%0];" ::"l"(a.rowgid + ((long long)seq * ntp + warp) * kBM));
     asm volatile("prefetch.global.L2 [%0];" ::"l"(a.part + (long long)b0 * pst + (long long)node * kBM));
   }
+  // round 0's addresses (index math only) before the wait
+  int S = 0, base = 0;
+  bool on = warp < ntp;
+  if (on) tile_units(a, global_tile(a, seq, warp), S, base);
   pdl_wait();  // A complete: partials, row ids (and the fused step's drop bitmap) visible
   asm volatile("griddepcontrol.launch_dependents;");
   if (tid == 0) trace_b(a, 1);
@@ -520,9 +552,12 @@ __global__ void __launch_bounds__(kBThreads, 1) head_select_kernel(const __grid_
     const int treg = (mrow + kBM - 1) / kBM;
     if (v0 > 0 && v0 >= treg && v0 + kRoundTiles <= a.tps) continue;  // a chunk of tiles past n_active
     const int tile = v0 + warp;  // regular tiles [0, tps), then patch tiles
-    const bool on = tile < ntp && !(v0 > 0 && tile >= treg && tile < a.tps);
-    int S = 0, base = 0;
-    if (on) tile_units(a, global_tile(a, seq, tile), S, base);
+    if (v0 > 0) {
+      on = tile < ntp && !(tile >= treg && tile < a.tps);
+      S = 0;
+      base = 0;
+      if (on) tile_units(a, global_tile(a, seq, tile), S, base);
+    }
     const int4 g4 = on ? __ldcg(reinterpret_cast<const int4*>(a.rowgid + ((long long)seq * ntp + tile) * kBM) + lane)
                        : make_int4(-1, -1, -1, -1);
     const uint32_t dw = (on && a.drop) ? __ldcg(&a.drop[tile * 4 + (lane >> 3)]) >> ((lane & 7) * 4) : 0u;
@@ -685,6 +720,7 @@ SplitLayout split_layout(int batch, int max_ids, int n, int num_sms) {
 }
 
 int g_split_pdl = 1;
+int g_stream_only = 0;  // debug mode 1: kernel A alone (measurement; no outputs are written)
 // experiments (NANOSPEC_SPLIT_FLAGS): 1 = skip kernel B, 2 = no PDL, 4 = kernel B twice,
 // 8 = W rows with an L2 evict-first policy, 16 = kernel B alone
 int g_split_flags = -1;
@@ -750,7 +786,7 @@ cudaError_t launch_pair_of_kernels(const SplitArgs& a, int grid_a, cudaStream_t 
   b.trace_base = grid_a;
   if (!(split_flags() & 16)) {  // experiment 16: kernel B alone (on the previous call's partials)
     e = launch_ex(head_stream_kernel<NT, FUSED>, dim3(grid_a), kAThreads, ACfg<NT>::kSmemBytes, stream, a);
-    if (e != cudaSuccess || (split_flags() & 1)) return e;
+    if (e != cudaSuccess || (split_flags() & 1) || g_stream_only) return e;
   }
   e = launch_ex(head_select_kernel, dim3(a.p.batch * a.p.n), kBThreads, 0, stream, b);
   if (e != cudaSuccess || !(split_flags() & 4)) return e;
@@ -793,9 +829,12 @@ bool shape_ok(const HeadProblem& p, int k) {
 
 }  // namespace
 
-size_t head_split_scratch_bytes(int batch, int max_ids, int n) { return split_layout(batch, max_ids, n, 256).total; }
+size_t head_tc_scratch_bytes(int batch, int max_ids, int n) { return split_layout(batch, max_ids, n, 256).total; }
 
-void set_head_split_pdl(int on) { g_split_pdl = on; }
+void set_head_tc_mode(int mode) {
+  g_split_pdl = mode == 0 ? 0 : 1;
+  g_stream_only = mode == 1 ? 1 : 0;
+}
 
 // Splits: U units on the SMs; every tile takes S = U / tiles K splits and the
 // first U % tiles tiles one more (S = 1 and a persistent loop when the tiles
@@ -811,8 +850,8 @@ void plan_splits(SplitArgs& a, int U, int KB) {
   a.units = nt * S + extra;
 }
 
-cudaError_t launch_head_split(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse,
-                             void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t stream) {
+cudaError_t launch_head_tc(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse,
+                           void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t stream) {
   if (!shape_ok(p, k)) return cudaErrorNotSupported;
   const int G = num_sms < 256 ? num_sms : 256;
   const SplitLayout L = split_layout(p.batch, p.max_ids, p.n, 256);
@@ -825,7 +864,7 @@ cudaError_t launch_head_split(const HeadProblem& p, int k, float* topk_logit, in
   return launch_nt<false>(a, a.heads, stream);
 }
 
-cudaError_t launch_step_split(const HeadProblem& p, const AppendArgs& upd, int k, float* topk_logit,
+cudaError_t launch_step_tc(const HeadProblem& p, const AppendArgs& upd, int k, float* topk_logit,
                               int32_t* topk_id, float* lse, void* scratch, size_t scratch_bytes, int num_sms,
                               cudaStream_t stream, bool dry_run) {
   if (!shape_ok(p, k) || p.batch != 1) return cudaErrorNotSupported;

@@ -36,60 +36,29 @@ unsigned long long* trace_buffer();
 
 // Phase 1 (a3+a4): gathered contraction into the fp32 logits staging buffer.
 cudaError_t launch_head_simt(const HeadProblem& p, int num_sms, cudaStream_t stream);
-// Tensor-core variant, a3+a4+a5 fused in one kernel (writes the top-k, lse and,
-// if p.logits != null, the debug logits).  Returns cudaErrorNotSupported when
-// the shape is not covered (the caller falls back to SIMT only for AUTO).
+// Tensor-core head, a3+a4+a5 (head_split.cu): stream kernel A (gather +
+// tcgen05 UMMA, K-split partial tiles to L2) chained by programmatic dependent
+// launch to select kernel B (sum in K order, top-k, lse; writes the top-k, lse
+// and, if p.logits != null, the debug logits).  Returns cudaErrorNotSupported
+// when the shape is not covered (the caller falls back to SIMT only for AUTO).
 cudaError_t launch_head_tc(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse,
                            void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t stream);
 size_t head_tc_scratch_bytes(int batch, int max_ids, int n);
 struct AppendArgs;
 // Fused step: the fast-path update `upd` (one sequence, rule R1) and the head of
-// that sequence in one launch (p.batch == 1, p points at that sequence).
+// that sequence in one pair of launches (p.batch == 1, p points at that
+// sequence; p.logits != null: the streamed rows' logits, nanospec_step_debug).
 // cudaErrorNotSupported when the shape cannot be fused (caller: update + head).
 // dry_run: only decide (cudaSuccess = would fuse), launch nothing.
 cudaError_t launch_step_tc(const HeadProblem& p, const AppendArgs& upd, int k, float* topk_logit, int32_t* topk_id,
                            float* lse, void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t stream,
                            bool dry_run = false);
-// Pair-split tensor-core head (head_pair.cu): the one-wave regime (every row
-// tile resident at once).  Scratch shared with head_tc.cu's layout.
-constexpr int kMaxPairSMs = 256;
-struct PairScratch {
-  uint2* cand;          // pair_cand_bytes(n): row keys, ids, tile maxima and lse partials
-  unsigned* node_ctr;   // [batch * n], zero between launches
-  unsigned* grid_word;  // grid barrier word (generation << 12 | arrivals), shared with head_tc.cu
-  unsigned* step_ctr;   // fused: publication generation
-  unsigned* arrive_ctr; // fused: zero between launches
-  uint32_t* stale;      // fused: [max_ids / 32]
-  int32_t* enter_ids;   // fused: [kFastThreads]
-  int* enter_meta;      // fused: [4]
-};
-size_t pair_cand_bytes(int n);
-cudaError_t launch_head_pair(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse,
-                             const PairScratch& s, int num_sms, cudaStream_t stream);
-cudaError_t launch_step_pair(const HeadProblem& p, const AppendArgs& upd, int k, float* topk_logit,
-                             int32_t* topk_id, float* lse, const PairScratch& s, int num_sms, cudaStream_t stream,
-                             bool dry_run);
-void set_head_pair_enabled(int on);
-// Two-kernel head (head_split.cu): stream kernel A (gather + UMMA + partials to
-// L2) and select kernel B (sum + top-k + lse), chained by programmatic
-// dependent launch.  Scratch: head_split_scratch_bytes at the start of `scratch`.
-size_t head_split_scratch_bytes(int batch, int max_ids, int n);
-cudaError_t launch_head_split(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse,
-                              void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t stream);
-cudaError_t launch_step_split(const HeadProblem& p, const AppendArgs& upd, int k, float* topk_logit,
-                              int32_t* topk_id, float* lse, void* scratch, size_t scratch_bytes, int num_sms,
-                              cudaStream_t stream, bool dry_run);
-void set_head_split_pdl(int on);
-// The fused step through the split head only (the debug-logits call); scratch as launch_step_tc.
-cudaError_t launch_step_split_only(const HeadProblem& p, const AppendArgs& upd, int k, float* topk_logit,
-                                   int32_t* topk_id, float* lse, void* scratch, size_t scratch_bytes, int num_sms,
-                                   cudaStream_t stream);
 // Whether launch_state_append would take the per-step fast path for these lists.
 bool state_fast_path(const StateView& sv, int reset, long long a_len, int a_dedup, long long b_len, int b_dedup);
-// Debug: force the fused head's reduction mode (-1 auto, 0 finisher, 1 poll, 2 cluster).
+// Debug: -1 default; 0 = launch the head's kernels without programmatic
+// dependent launch (plain stream order); 1 = the stream kernel alone (timing
+// only: no outputs).
 void set_head_tc_mode(int mode);
-// Debug: cap the cluster (K-split) size the cluster / fused modes try (0 = no cap).
-void set_head_tc_cluster_cap(int s);
 
 // Phase 2 (a5): per (sequence, node) top-k by (value desc, id asc) + lse.
 cudaError_t launch_select_topk(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse,

@@ -1,4 +1,4 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-T=${TAG:-r2e}
+T=${TAG:-r2j}
 ( timeout 200 python scripts/split_dev.py --trace ) 2>&1 | grep -v Warn | tee gpurun_out/${T}_split.log

@@ -110,8 +110,8 @@ def test_static_32k_set(cuda_ok, llama):
     H = SI.bf16_hidden(n, d, seed=41, device="cuda")
     v, i, l, zz = logits_topk_ids(_t(ids), _t([len(ids)]), W, H, k, debug_logits=True)
     torch.cuda.synchronize()
-    _check(v.cpu().numpy(), i.cpu().numpy(), l.cpu().numpy(), ids, Wb, H, k, "static 32k set",
-           zz.reshape(n, -1)[:, : len(ids)].cpu().numpy())
+    _check(v[0].cpu().numpy(), i[0].cpu().numpy(), l[0].cpu().numpy(), ids, Wb, H, k, "static 32k set",
+           zz[0, :, : len(ids)].cpu().numpy())
 
 
 @pytest.mark.parametrize("regime", ["headline", "zipf"])

@@ -118,8 +118,8 @@ def test_step_small_window_and_invalid_ids(cuda_ok, llama):
 
 
 def test_step_fallback_tiny(cuda_ok):
-    """A shape the fused kernel does not take (d = 64: one K block, no split)
-    runs as update + head with the same results."""
+    """The tiny shape (d = 64: one K atom, so split-K 1) through nanospec_step:
+    the oracle's state and top-k every step."""
     from paper_2605_26444_b200 import ActiveVocab, step
     V, d, Wm, n, k = 1000, 64, 256, 8, 10
     W = SI.bf16_weights(V, d, seed=0, device="cuda")
@@ -138,15 +138,16 @@ def test_step_fallback_tiny(cuda_ok):
         _check_head(v, i, l, ids, Wb, H, k, f"tiny step {s}")
 
 
-@pytest.mark.parametrize("cap", [2, 3, 4, 6])
-def test_step_cluster_sizes(cuda_ok, llama, cap):
-    """The fused step with the cluster (K-split) size capped: every split count
-    gives the oracle's state and top-k."""
+@pytest.mark.parametrize("mode", [-1, 0])
+def test_step_launch_modes(cuda_ok, llama, mode):
+    """The fused step with (-1) and without (0) programmatic dependent launch
+    between its kernels: the oracle's state and top-k every step."""
     from paper_2605_26444_b200 import ActiveVocab, HeadOutputs, step, _native as N
     W, Wb = llama
     V, d = W.shape
     Wm, n, k = 3072, 60, 10
-    N.check(N.lib().nanospec_debug_set_cluster_cap(cap), "cluster cap")
+    cap = mode
+    N.check(N.lib().nanospec_debug_set_head_mode(mode), "head mode")
     try:
         z = SI.Zipf(V)
         prompt, pre = SI.prompt_and_prefill(z, 8, 1500, 3)
@@ -159,10 +160,10 @@ def test_step_cluster_sizes(cuda_ok, llama, cap):
             v, i, l = step(st, 0, _t(dd), _t(vv), W, H, k, out=out)
             torch.cuda.synchronize()
             ref.update(dd, vv)
-            ids = _check_state(st, ref, f"cap {cap} step {s}")
-            _check_head(v, i, l, ids, Wb, H, k, f"cap {cap} step {s}")
+            ids = _check_state(st, ref, f"mode {cap} step {s}")
+            _check_head(v, i, l, ids, Wb, H, k, f"mode {cap} step {s}")
     finally:
-        N.check(N.lib().nanospec_debug_set_cluster_cap(0), "cluster cap")
+        N.check(N.lib().nanospec_debug_set_head_mode(-1), "head mode")
 
 
 def test_step_many_back_to_back(cuda_ok, llama):
