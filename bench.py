@@ -397,11 +397,64 @@ def run_ours(args):
 
     extra["us_draft_round_1x1_5x10"] = timed(draft_round, max(R, K // 6))
 
+    # the whole device-side round: one n = 1 head call and five
+    # n = 10 calls, each followed by the EAGLE-2 expansion (cumulative
+    # log-softmax scores over I), the rerank to 60 draft tokens, and the fused
+    # decode step with those tokens as C_draft (+ 3 verify tokens)
+    trees = [P.DraftTree(1 + 10 * k + 5 * 10 * k, 10, dev) for _ in range(R)]
+    toks = [torch.empty(60, dtype=torch.int32, device=dev) for _ in range(R)]
+    tidx = [torch.empty(60, dtype=torch.int32, device=dev) for _ in range(R)]
+    ver3 = [upd_v[r][0].clone() for r in range(R)]
+
+    def tree_round(s):
+        r = s % R
+        tr = trees[r]
+        tr.reset()
+        P.draft_logits_topk(states[r], W, hn[1][0][r:r + 1], k, impl=args.head, out=hn[1][1][r])
+        tr.expand(hn[1][1][r].topk_logit[0], hn[1][1][r].topk_id[0], hn[1][1][r].lse[0], 10)
+        for _ in range(5):
+            P.draft_logits_topk(states[r], W, hn[10][0][r:r + 1], k, impl=args.head, out=hn[10][1][r])
+            tr.expand(hn[10][1][r].topk_logit[0], hn[10][1][r].topk_id[0], hn[10][1][r].lse[0], 10)
+        tr.rerank(60, tidx[r], toks[r])
+        P.step(states[r], 0, toks[r], ver3[r], W, Hs[r], k, out=outs[r])
+
+    if k <= 32 and 10 * k <= 1024:
+        snap2 = [st_.workspace.clone() for st_ in states]
+        extra["us_draft_round_tree_and_step"] = timed(tree_round, max(R, K // 8))
+        for st_, sn in zip(states, snap2):  # the headline recipe needs the fresh-pool state back
+            st_.workspace.copy_(sn)
+        del snap2
+
     # the stream kernel alone (gather + contraction, partials to L2; no select)
     from paper_2605_26444_b200 import _native as N
     N.check(N.lib().nanospec_debug_set_head_mode(1), "head mode")
     extra["us_stream_kernel_alone"] = timed(head_only, K)
     N.check(N.lib().nanospec_debug_set_head_mode(args.head_mode), "head mode")
+
+    # the paper's repack design: the head over a dense
+    # packed copy of the active rows, and a step as update + delta repack (the
+    # slots whose id changed) + packed head, all on one stream (no backbone to
+    # hide the copy behind)
+    packs = [P.PackedHead(states[r], d, dev) for r in range(R)]
+    for r in range(R):
+        packs[r].refresh(0, W)
+    torch.cuda.synchronize()
+    extra["us_head_packed_rows"] = timed(lambda s: packs[s % R].head(Hs[s % R:s % R + 1], k, outs[s % R]), K)
+    snap3 = [st_.workspace.clone() for st_ in states]
+
+    def repack_step(s):
+        r = s % R
+        c = cursor[r]
+        cursor[r] += 1
+        states[r].update(0, upd_d[r][c], upd_v[r][c])
+        packs[r].refresh(0, W)
+        packs[r].head(Hs[r:r + 1], k, outs[r])
+
+    extra["us_step_repack_variant"] = timed(repack_step, K)
+    extra["us_repack_delta_alone"] = timed(lambda s: packs[s % R].refresh(0, W), K)
+    for st_, sn in zip(states, snap3):
+        st_.workspace.copy_(sn)
+    del snap3, packs
 
     # natural active sets: each of R sequences holds the window of
     # a 3072-token Zipf(s = 1.0) stream (~1.7k distinct ids), head only, cold L2
@@ -551,7 +604,13 @@ def run_ours(args):
                      "kernel": ("the fused step: stream kernel (update + gather + contraction) + select kernel "
                                 "(top-k + lse), per step" if fused
                                 else "draft_logits_topk call (contraction + top-k select)"),
-                     "alg_bytes_per_launch": alg_bytes},
+                     "alg_bytes_per_launch": alg_bytes,
+                     "traffic_note": "dram bytes of the stream kernel per launch (ncu, profiles/traffic.json)",
+                     "stream_kernel": {"us_per_launch": extra.get("us_stream_kernel_alone"),
+                                       "achieved_gbps": round(alg_bytes / (extra["us_stream_kernel_alone"] * 1e-6) / 1e9, 1)
+                                       if extra.get("us_stream_kernel_alone") else None,
+                                       "frac": round(alg_bytes / (extra["us_stream_kernel_alone"] * 1e-6) / 1e9 / peak, 4)
+                                       if extra.get("us_stream_kernel_alone") else None}},
         "dense": {kk: (round(vv, 3) if isinstance(vv, float) else vv) for kk, vv in dense.items()},
         "paper_context": {"draft_time_cut": "51.6% vs EAGLE-2 (Llama-3.1-8B-Instruct, P:55, P:383)",
                           "end_to_end_speedup": "1.17-1.29x over EAGLE-2, 1.19-1.28x over EAGLE-3 (P:55, P:122)",
@@ -721,12 +780,53 @@ def run_vp32k(args):
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for i in range(args.steps):
-        step(args.warmup + i)
-    e1.record(stream)
+    # the whole VP step (update, local head, all-gather, merge) captured in one
+    # graph when the collective allows it, else eager
+    timing = "one CUDA graph of the step (update + local head + NCCL all-gather + merge)"
+    try:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for i in range(args.steps):
+                step(args.warmup + i)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0.record(stream)
+        g.replay()
+        e1.record(stream)
+    except Exception as ex:  # capture of the collective refused: eager launches
+        timing = f"eager launches ({type(ex).__name__} capturing the step)"
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0.record(stream)
+        for i in range(args.steps):
+            step(args.warmup + i)
+        e1.record(stream)
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / args.steps
+    # breakdown: local head alone, the candidate all-gather alone, the merge alone
+    brk = {}
+    reps = 20
+
+    def t_of(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return round(e0.elapsed_time(e1) * 1e3 / reps, 3)
+
+    brk["us_local_head"] = t_of(lambda: P.draft_logits_topk(st, Wl, H, k, impl=args.head, out=out))
+    if world > 1:
+        v0, i0, l0 = out.topk_logit[0], out.topk_id[0], out.lse[0]
+        brk["us_allgather"] = t_of(lambda: PAR.gather_candidates(v0, i0, l0))
+        cl, ci, cls = PAR.gather_candidates(v0, i0, l0)
+        brk["us_merge"] = t_of(lambda: P.merge_topk(cl, ci, cls, k))
+        brk["allgather_bytes_per_rank"] = int(PAR.pack_candidates(v0, i0, l0).numel() * 4)
     if world > 1:
         t = torch.tensor([us], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -737,7 +837,8 @@ def run_vp32k(args):
             "config": {"workload": f"vp32k: llama-3.1-8b head, W_max={Wm} Zipf window, n={n} k={k}",
                        "active_ids_rank0": n_act, "parallelism": f"vp{world} (cyclic vocab shards, NCCL all-gather "
                                                                f"of per-shard top-k + lse, exact merge)",
-                       "timing": "eager launches (the all-gather is not graph-captured)", "head": args.head}}
+                       "timing": timing, "head": args.head},
+            "breakdown": brk}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

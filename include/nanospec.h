@@ -269,6 +269,51 @@ nanospec_status nanospec_step_host(nanospec_state st, int32_t seq, const void* h
 int32_t nanospec_step_fused(const nanospec_state st, int32_t n_draft, int32_t k_ver, int32_t d_model,
                             int32_t n_nodes, int32_t k);
 
+/* The paper's repack design (T6 `repack_buf`), built as a
+ * measured alternative to the fused direct gather.
+ * nanospec_repack: for every slot j < n_active of sequence `seq` whose tag
+ * differs from ids[j], copy row W_head[ids[j]] (d_model bf16) into packed row
+ * j and set the tag -- after an update that is the delta of the entering
+ * ids.  d_packed bf16 [batch x w_max x ldp] and d_tags int32 [batch x w_max]
+ * (all -1 initially) are caller-owned; run it on a copy stream and order the
+ * packed head after it with an event.
+ * nanospec_draft_logits_topk_packed: nanospec_draft_logits_topk (tensor-core
+ * head) with every active row read from its packed slot instead of W_head --
+ * contiguous rows; results identical.  Asynchronous; EINVAL on bad arguments,
+ * EUNSUPPORTED where the tensor-core head does not take the shape. */
+nanospec_status nanospec_repack(const nanospec_state st, int32_t seq, const void* d_w_head, int32_t d_model,
+                                int64_t ldw, void* d_packed, int64_t ldp, int32_t* d_tags, cudaStream_t stream);
+nanospec_status nanospec_draft_logits_topk_packed(const nanospec_state st, const void* d_packed, int32_t d_model,
+                                                  int64_t ldp, const void* d_hidden, int32_t n_nodes, int32_t k,
+                                                  float* d_topk_logit, int32_t* d_topk_id, float* d_lse,
+                                                  void* d_scratch, size_t scratch_bytes, cudaStream_t stream);
+
+/* Draft-tree bookkeeping of one EAGLE-2-style round (the
+ * SelectDraftTokens loop of Alg. 1; tree depth 5 / 60 draft tokens,
+ * P:286), on the device so a whole round is one CUDA graph.
+ *
+ * nanospec_tree_expand: the k children of each of the n_front frontier nodes
+ * (the head's top-k over I: d_topk_logit / d_topk_id [n_front x k], d_lse
+ * [n_front]) are appended to a node pool at pool_offset with cumulative score
+ * s_parent + (z - lse_parent) -- the log-softmax over the active set;
+ * the root has d_front_score = d_front_index = NULL (score 0, parent -1).
+ * The n_next best children of the level (score desc, pool index asc) are
+ * written as the next frontier (d_next_index: pool indices, d_next_score).
+ * Padding children (id -1) score -inf.  n_front * k <= 1024; pool_offset +
+ * n_front * k <= pool_cap <= 4096.  Pool arrays: d_pool_score fp32,
+ * d_pool_id / d_pool_parent int32 [pool_cap], caller-owned.
+ *
+ * nanospec_tree_rerank: the m best nodes of pool[0, pool_n) (same order):
+ * d_out_index = their pool indices, d_out_id = their token ids (C_draft).
+ * Both asynchronous on `stream`; EINVAL on bad sizes. */
+nanospec_status nanospec_tree_expand(const float* d_front_score, const int32_t* d_front_index, int32_t n_front,
+                                     const float* d_topk_logit, const int32_t* d_topk_id, const float* d_lse,
+                                     int32_t k, float* d_pool_score, int32_t* d_pool_id, int32_t* d_pool_parent,
+                                     int32_t pool_offset, int32_t pool_cap, int32_t n_next, int32_t* d_next_index,
+                                     float* d_next_score, cudaStream_t stream);
+nanospec_status nanospec_tree_rerank(const float* d_pool_score, const int32_t* d_pool_id, int32_t pool_n, int32_t m,
+                                     int32_t* d_out_index, int32_t* d_out_id, cudaStream_t stream);
+
 /* Debug: phase trace.  d_buf = device uint64[ctas * 16] (ctas >= 256; rows for
  * the stream kernel's grid plus the select kernel's) or NULL (off, the
  * default).  While set, the tensor-core head writes %globaltimer (ns) marks:

@@ -223,3 +223,56 @@ void oracle_lse(const double* z, int32_t n_ids, int32_t n, double* lse_out) {
     lse_out[i] = m + log(s);
   }
 }
+
+/* EAGLE-2 draft-tree bookkeeping (SelectDraftTokens / "append x_draft to draft
+ * tree", Alg. 1; depth 5 and at most 60 draft tokens).
+ * Level expansion: child (f, j) of frontier node f gets the cumulative
+ * log-probability parent_score[f] + (val[f][j] - lse[f]) -- the log-softmax
+ * over the active set; the root has parent_score == NULL (score 0,
+ * parent -1).  Children are appended to the pool at pool_n in (f, j) order;
+ * padding children (id < 0) score -inf.  The n_next best children of this
+ * level, by (score desc, pool index asc), become the next frontier: repeated
+ * arg-max, plain loops. */
+void oracle_tree_expand(const double* parent_score, const int32_t* parent_index, int32_t n_front,
+                        const double* val, const int32_t* id, const double* lse, int32_t k, double* pool_score,
+                        int32_t* pool_id, int32_t* pool_parent, int32_t pool_n, int32_t n_next,
+                        int32_t* next_index, double* next_score) {
+  const int32_t nc = n_front * k;
+  for (int32_t f = 0; f < n_front; ++f)
+    for (int32_t j = 0; j < k; ++j) {
+      const int32_t c = pool_n + f * k + j;
+      const int32_t tok = id[(int64_t)f * k + j];
+      const double ps = parent_score ? parent_score[f] : 0.0;
+      pool_score[c] = tok >= 0 ? ps + (val[(int64_t)f * k + j] - lse[f]) : -INFINITY;
+      pool_id[c] = tok;
+      pool_parent[c] = parent_index ? parent_index[f] : -1;
+    }
+  char* taken = (char*)calloc((size_t)(nc > 0 ? nc : 1), 1);
+  for (int32_t r = 0; r < n_next; ++r) {
+    int32_t best = -1;
+    for (int32_t c = 0; c < nc; ++c) {
+      if (taken[c]) continue;
+      if (best < 0 || pool_score[pool_n + c] > pool_score[pool_n + best]) best = c;  /* ties: lower index kept */
+    }
+    taken[best] = 1;
+    next_index[r] = pool_n + best;
+    next_score[r] = pool_score[pool_n + best];
+  }
+  free(taken);
+}
+
+/* Rerank: the m best nodes of the pool by (score desc, pool index asc): the
+ * draft tree, whose tokens form C_draft.  Repeated arg-max. */
+void oracle_tree_rerank(const double* pool_score, int32_t n, int32_t m, int32_t* out_index) {
+  char* taken = (char*)calloc((size_t)(n > 0 ? n : 1), 1);
+  for (int32_t r = 0; r < m; ++r) {
+    int32_t best = -1;
+    for (int32_t c = 0; c < n; ++c) {
+      if (taken[c]) continue;
+      if (best < 0 || pool_score[c] > pool_score[best]) best = c;
+    }
+    taken[best] = 1;
+    out_index[r] = best;
+  }
+  free(taken);
+}

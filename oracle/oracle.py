@@ -62,6 +62,11 @@ def lib():
         L.oracle_topk.restype = None
         L.oracle_lse.argtypes = [f64p, ctypes.c_int32, ctypes.c_int32, f64p]
         L.oracle_lse.restype = None
+        L.oracle_tree_expand.argtypes = [f64p, i32p, ctypes.c_int32, f64p, i32p, f64p, ctypes.c_int32, f64p, i32p,
+                                         i32p, ctypes.c_int32, ctypes.c_int32, i32p, f64p]
+        L.oracle_tree_expand.restype = None
+        L.oracle_tree_rerank.argtypes = [f64p, ctypes.c_int32, ctypes.c_int32, i32p]
+        L.oracle_tree_rerank.restype = None
         _lib = L
     return _lib
 
@@ -186,6 +191,48 @@ def lse(z):
     out, po = _f64(np.empty(n))
     lib().oracle_lse(pz, m, n, po)
     return out
+
+
+class OracleTree:
+    """EAGLE-2 draft-tree node pool (Alg. 1; log-softmax over I,
+    P:337): expand() one level from the head's top-k / lse of the frontier,
+    rerank() the best m nodes.  Marshalling only (oracle.c does the arithmetic)."""
+
+    def __init__(self, cap: int):
+        self.score = np.full(cap, -np.inf)
+        self.id = np.full(cap, -1, np.int32)
+        self.parent = np.full(cap, -1, np.int32)
+        self.n = 0
+        self.front_index = None
+        self.front_score = None
+
+    def expand(self, val, ids, lse, n_next: int, front_score=None, front_index=None):
+        val = np.ascontiguousarray(np.asarray(val, np.float64))
+        n_front, k = val.shape
+        ids_, pi = _i32(np.asarray(ids, np.int32).reshape(-1))
+        v_, pv = _f64(val)
+        l_, pl = _f64(np.asarray(lse, np.float64).reshape(-1))
+        fs = self.front_score if front_score is None else np.asarray(front_score, np.float64)
+        fi = self.front_index if front_index is None else np.asarray(front_index, np.int32)
+        root = self.n == 0
+        fs_, pfs = (None, None) if root else _f64(fs)
+        fi_, pfi = (None, None) if root else _i32(fi)
+        ps_, pps = _f64(self.score)
+        pid_, ppid = _i32(self.id)
+        ppar_, pppar = _i32(self.parent)
+        ni_, pni = _i32(np.zeros(max(n_next, 1), np.int32))
+        ns_, pns = _f64(np.zeros(max(n_next, 1)))
+        lib().oracle_tree_expand(pfs, pfi, n_front, pv, pi, pl, k, pps, ppid, pppar, self.n, n_next, pni, pns)
+        self.score, self.id, self.parent = ps_, pid_, ppar_
+        self.n += n_front * k
+        self.front_index, self.front_score = ni_[:n_next].copy(), ns_[:n_next].copy()
+        return self.front_index, self.front_score
+
+    def rerank(self, m: int):
+        s_, ps = _f64(self.score[: self.n].copy())
+        o_, po = _i32(np.zeros(m, np.int32))
+        lib().oracle_tree_rerank(ps, self.n, m, po)
+        return o_.copy(), self.id[o_].copy()
 
 
 class OracleStream:

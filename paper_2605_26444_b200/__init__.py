@@ -13,7 +13,9 @@ _lib()  # fail loudly at import if the native library is missing
 
 from .nanospec import (  # noqa: E402
     ActiveVocab,
+    DraftTree,
     HeadOutputs,
+    PackedHead,
     draft_logits_topk,
     head_scratch_bytes,
     logits_topk_ids,
@@ -27,6 +29,6 @@ from .nanospec import (  # noqa: E402
 )
 
 __all__ = [
-    "ActiveVocab", "HeadOutputs", "draft_logits_topk", "logits_topk_ids", "merge_topk",
+    "ActiveVocab", "DraftTree", "HeadOutputs", "PackedHead", "draft_logits_topk", "logits_topk_ids", "merge_topk",
     "head_scratch_bytes", "state_workspace_bytes", "step", "step_debug", "step_host", "StepHostIO", "step_is_fused",
 ]

@@ -264,7 +264,7 @@ nanospec_status nanospec_draft_logits_topk_ex(const nanospec_state st, const voi
   if (!aligned16(d_w_head) || !aligned16(d_hidden)) return NANOSPEC_EINVAL;
   if (impl != NANOSPEC_HEAD_AUTO && impl != NANOSPEC_HEAD_SIMT && impl != NANOSPEC_HEAD_TC) return NANOSPEC_EINVAL;
   const StateView& sv = st->sv;
-  HeadProblem hp;
+  HeadProblem hp = {};
   hp.w = (const uint16_t*)d_w_head;
   hp.ldw = ldw;
   hp.d = d_model;
@@ -305,7 +305,7 @@ nanospec_status step_impl(nanospec_state st, int32_t seq, const int32_t* d_draft
   if (!aligned16(d_w_head) || !aligned16(d_hidden)) return NANOSPEC_EINVAL;
   const StateView& sv = st->sv;
   if (!d_scratch || scratch_bytes < nanospec_head_scratch_bytes(1, sv.w_max, n_nodes)) return NANOSPEC_EINVAL;
-  HeadProblem hp;
+  HeadProblem hp = {};
   hp.w = (const uint16_t*)d_w_head;
   hp.ldw = ldw;
   hp.d = d_model;
@@ -427,7 +427,7 @@ nanospec_status nanospec_logits_topk_ids(const int32_t* d_ids, const int32_t* d_
   if (n_nodes < 1 || n_nodes > NANOSPEC_MAX_NODES || k < 1 || k > NANOSPEC_MAX_K) return NANOSPEC_EINVAL;
   if (!aligned16(d_w_head) || !aligned16(d_hidden)) return NANOSPEC_EINVAL;
   if (impl != NANOSPEC_HEAD_AUTO && impl != NANOSPEC_HEAD_SIMT && impl != NANOSPEC_HEAD_TC) return NANOSPEC_EINVAL;
-  HeadProblem hp;
+  HeadProblem hp = {};
   hp.w = (const uint16_t*)d_w_head;
   hp.ldw = ldw;
   hp.d = d_model;
@@ -465,6 +465,79 @@ nanospec_status nanospec_merge_topk(const float* d_cand_logit, const int32_t* d_
   if (d_out_lse && !d_cand_lse) return NANOSPEC_EINVAL;
   return cuda_status(launch_merge_topk(d_cand_logit, d_cand_id, d_cand_lse, n_shards, n_rows, k, d_out_logit,
                                        d_out_id, d_out_lse, stream));
+}
+
+nanospec_status nanospec_repack(const nanospec_state st, int32_t seq, const void* d_w_head, int32_t d_model,
+                                int64_t ldw, void* d_packed, int64_t ldp, int32_t* d_tags, cudaStream_t stream) {
+  if (!st || seq < 0 || seq >= st->sv.batch || !d_w_head || !d_packed || !d_tags) return NANOSPEC_EINVAL;
+  if (d_model <= 0 || d_model % 8 != 0 || ldw < d_model || ldw % 8 != 0 || ldp < d_model || ldp % 8 != 0)
+    return NANOSPEC_EINVAL;
+  if (!aligned16(d_w_head) || !aligned16(d_packed)) return NANOSPEC_EINVAL;
+  return cuda_status(launch_repack(st->sv, seq, (const uint16_t*)d_w_head, ldw, d_model, (uint16_t*)d_packed, ldp,
+                                   d_tags, stream));
+}
+
+nanospec_status nanospec_draft_logits_topk_packed(const nanospec_state st, const void* d_packed, int32_t d_model,
+                                                  int64_t ldp, const void* d_hidden, int32_t n_nodes, int32_t k,
+                                                  float* d_topk_logit, int32_t* d_topk_id, float* d_lse,
+                                                  void* d_scratch, size_t scratch_bytes, cudaStream_t stream) {
+  if (!st || !d_packed || !d_hidden || !d_topk_logit || !d_topk_id) return NANOSPEC_EINVAL;
+  if (d_model <= 0 || d_model % 8 != 0 || ldp < d_model || ldp % 8 != 0) return NANOSPEC_EINVAL;
+  if (n_nodes < 1 || n_nodes > NANOSPEC_MAX_NODES || k < 1 || k > NANOSPEC_MAX_K) return NANOSPEC_EINVAL;
+  if (!aligned16(d_packed) || !aligned16(d_hidden)) return NANOSPEC_EINVAL;
+  const StateView& sv = st->sv;
+  HeadProblem hp = {};
+  hp.w = (const uint16_t*)d_packed;  // not dereferenced: rows come from `packed`
+  hp.ldw = ldp;
+  hp.d = d_model;
+  hp.h = (const uint16_t*)d_hidden;
+  hp.n = n_nodes;
+  hp.batch = sv.batch;
+  hp.ids_base = sv.ids;
+  hp.ids_stride = sv.w_max;
+  hp.nact_base = &sv.meta[0].n_active;
+  hp.nact_stride = sizeof(Meta) / sizeof(int32_t);
+  hp.max_ids = sv.w_max;
+  hp.n_shards = sv.n_shards;
+  hp.trace = trace_buffer();
+  hp.packed = (const uint16_t*)d_packed;
+  hp.ldp = ldp;
+  return run_head(hp, k, d_topk_logit, d_topk_id, d_lse, nullptr, d_scratch, scratch_bytes, NANOSPEC_HEAD_TC, stream);
+}
+
+nanospec_status nanospec_tree_expand(const float* d_front_score, const int32_t* d_front_index, int32_t n_front,
+                                     const float* d_topk_logit, const int32_t* d_topk_id, const float* d_lse,
+                                     int32_t k, float* d_pool_score, int32_t* d_pool_id, int32_t* d_pool_parent,
+                                     int32_t pool_offset, int32_t pool_cap, int32_t n_next, int32_t* d_next_index,
+                                     float* d_next_score, cudaStream_t stream) {
+  if (!d_topk_logit || !d_topk_id || !d_lse || !d_pool_score || !d_pool_id || !d_pool_parent) return NANOSPEC_EINVAL;
+  if ((d_front_score == nullptr) != (d_front_index == nullptr)) return NANOSPEC_EINVAL;
+  if (n_front < 1 || k < 1 || k > NANOSPEC_MAX_K || n_front * k > 1024 || pool_offset < 0) return NANOSPEC_EINVAL;
+  if ((long long)pool_offset + (long long)n_front * k > pool_cap || pool_cap > 4096) return NANOSPEC_EINVAL;
+  if (n_next < 0 || n_next > n_front * k || (n_next > 0 && (!d_next_index || !d_next_score))) return NANOSPEC_EINVAL;
+  TreeLevel t;
+  t.front_score = d_front_score;
+  t.front_index = d_front_index;
+  t.topk_logit = d_topk_logit;
+  t.topk_id = d_topk_id;
+  t.lse = d_lse;
+  t.n_front = n_front;
+  t.k = k;
+  t.pool_score = d_pool_score;
+  t.pool_id = d_pool_id;
+  t.pool_parent = d_pool_parent;
+  t.pool_offset = pool_offset;
+  t.n_next = n_next;
+  t.next_index = d_next_index;
+  t.next_score = d_next_score;
+  return cuda_status(launch_tree_expand(t, stream));
+}
+
+nanospec_status nanospec_tree_rerank(const float* d_pool_score, const int32_t* d_pool_id, int32_t pool_n, int32_t m,
+                                     int32_t* d_out_index, int32_t* d_out_id, cudaStream_t stream) {
+  if (!d_pool_score || !d_pool_id || !d_out_index || !d_out_id) return NANOSPEC_EINVAL;
+  if (pool_n < 1 || pool_n > 4096 || m < 1 || m > pool_n) return NANOSPEC_EINVAL;
+  return cuda_status(launch_tree_rerank(d_pool_score, d_pool_id, pool_n, m, d_out_index, d_out_id, stream));
 }
 
 }  // extern "C"

@@ -351,7 +351,9 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
           const int r = lr + 64 * i;
           const int32_t g = r < rows ? ids_s[buf][r] : -1;
           const long long row = p.n_shards > 1 ? g / p.n_shards : g;
-          rp[i] = g >= 0 ? p.w + row * p.ldw + (tid & 7) * 8 : nullptr;
+          const uint16_t* base = p.packed ? p.packed + ((long long)un.seq * p.max_ids + un.tile * kBM + r) * p.ldp
+                                          : p.w + row * p.ldw;  // repacked rows: contiguous slots
+          rp[i] = g >= 0 ? base + (tid & 7) * 8 : nullptr;
         }
         const uint16_t* hp = p.h + (long long)un.seq * p.n * p.d + (tid & 7) * 8;
         uint64_t pol = 0;

@@ -29,7 +29,17 @@ struct HeadProblem {
   int n_shards;             // row(g) = g / n_shards
   float* logits;            // fp32 [batch x n x max_ids]
   unsigned long long* trace; // debug phase trace or null
+  const uint16_t* packed;   // repacked rows or null: slot j of sequence b at packed + (b * max_ids + j) * ldp
+  long long ldp;
 };
+
+// The paper's repack (T6 `repack_buf` P:451) as a measured variant:
+// copy W_head[ids[j]] into packed row j for every slot j < n_active whose tag
+// (the id the packed row holds) differs from ids[j] -- the delta of one update
+// is the entering ids' slots -- and update the tags.  tags: int32 [w_max] per
+// sequence, -1 initially.
+cudaError_t launch_repack(const StateView& sv, int seq, const uint16_t* w, long long ldw, int d, uint16_t* packed,
+                          long long ldp, int32_t* tags, cudaStream_t stream);
 
 // Debug phase-trace buffer (nanospec_debug_set_trace); null = off.
 unsigned long long* trace_buffer();
@@ -63,6 +73,26 @@ void set_head_tc_mode(int mode);
 // Phase 2 (a5): per (sequence, node) top-k by (value desc, id asc) + lse.
 cudaError_t launch_select_topk(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse,
                                cudaStream_t stream);
+
+// Draft-tree bookkeeping (tree.cu).
+struct TreeLevel {
+  const float* front_score;   // [n_front] cumulative log-probabilities (null: the root, 0)
+  const int32_t* front_index; // [n_front] pool indices of the frontier nodes (null: the root, parent -1)
+  const float* topk_logit;    // [n_front][k] the head's top-k over I
+  const int32_t* topk_id;
+  const float* lse;           // [n_front] lse over I
+  int n_front, k;
+  float* pool_score;          // the node pool: children appended at pool_offset
+  int32_t* pool_id;
+  int32_t* pool_parent;
+  int pool_offset;
+  int n_next;                 // children kept as the next frontier
+  int32_t* next_index;        // [n_next] pool indices, best first
+  float* next_score;          // [n_next]
+};
+cudaError_t launch_tree_expand(const TreeLevel& t, cudaStream_t stream);
+cudaError_t launch_tree_rerank(const float* score, const int32_t* id, int n, int m, int32_t* out_index,
+                               int32_t* out_id, cudaStream_t stream);
 
 cudaError_t launch_merge_topk(const float* cand_logit, const int32_t* cand_id, const float* cand_lse,
                               int n_shards, int n_rows, int k, float* out_logit, int32_t* out_id, float* out_lse,

@@ -280,12 +280,14 @@ cudaError_t launch_select_topk(const HeadProblem& p, int k, float* topk_logit, i
   dim3 grid(p.n, p.batch);
   if (p.max_ids <= kStageCap) {
     size_t smem = (size_t)p.max_ids * sizeof(float);
-    static bool attr_set = false;
-    if (!attr_set) {
+    static bool attr_set[64] = {false};  // the attribute is per (function, device)
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (!attr_set[dev]) {
       cudaError_t e = cudaFuncSetAttribute(select_topk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            kStageCap * (int)sizeof(float));
       if (e != cudaSuccess) return e;
-      attr_set = true;
+      attr_set[dev] = true;
     }
     select_topk_kernel<true><<<grid, kSelThreads, smem, stream>>>(p, o);
   } else {

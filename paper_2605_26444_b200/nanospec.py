@@ -345,3 +345,79 @@ def merge_topk(cand_logit: torch.Tensor, cand_id: torch.Tensor, cand_lse: torch.
     N.check(N.lib().nanospec_merge_topk(_ptr(cand_logit), _ptr(cand_id), _ptr(cand_lse), S, rows, k, _ptr(ol),
                                         _ptr(oi), _ptr(olse), _stream(cand_logit.device)), "nanospec_merge_topk")
     return ol, oi, olse
+
+
+class DraftTree:
+    """Device node pool of one EAGLE-2-style draft round (Alg. 1
+    P:523-530; depth 5 and 60 draft tokens): expand() appends a level's
+    children with cumulative log-probability scores (log-softmax over I,
+    P:337) and picks the next frontier; rerank() keeps the best `m` nodes --
+    their tokens are C_draft of the state update.  Fixed
+    buffers, so a whole round can be captured in one CUDA graph."""
+
+    def __init__(self, pool_cap: int, width: int, device):
+        if not 1 <= pool_cap <= 4096:
+            raise ValueError("pool_cap must be in [1, 4096]")
+        self.cap, self.width = pool_cap, width
+        self.score = torch.full((pool_cap,), float("-inf"), dtype=torch.float32, device=device)
+        self.id = torch.full((pool_cap,), -1, dtype=torch.int32, device=device)
+        self.parent = torch.full((pool_cap,), -1, dtype=torch.int32, device=device)
+        self.front_index = torch.zeros(width, dtype=torch.int32, device=device)
+        self.front_score = torch.zeros(width, dtype=torch.float32, device=device)
+        self.n = 0
+        self.n_front = 0
+
+    def reset(self):
+        self.n = 0
+        self.n_front = 0
+
+    def expand(self, topk_logit: torch.Tensor, topk_id: torch.Tensor, lse: torch.Tensor, n_next: int):
+        """One level: the head outputs of the current frontier (root when the
+        pool is empty) -> children in the pool, the best n_next as the frontier."""
+        n_front, k = topk_logit.shape[-2], topk_logit.shape[-1]
+        root = self.n == 0
+        st = N.lib().nanospec_tree_expand(
+            None if root else _ptr(self.front_score), None if root else _ptr(self.front_index), n_front,
+            _ptr(topk_logit), _ptr(topk_id), _ptr(lse), k, _ptr(self.score), _ptr(self.id), _ptr(self.parent),
+            self.n, self.cap, n_next, _ptr(self.front_index), _ptr(self.front_score), _stream(topk_logit.device))
+        N.check(st, "nanospec_tree_expand")
+        self.n += n_front * k
+        self.n_front = n_next
+
+    def rerank(self, m: int, out_index: torch.Tensor | None = None, out_id: torch.Tensor | None = None):
+        """The m best nodes of the pool: (pool indices [m], token ids [m])."""
+        dev = self.score.device
+        out_index = torch.empty(m, dtype=torch.int32, device=dev) if out_index is None else out_index
+        out_id = torch.empty(m, dtype=torch.int32, device=dev) if out_id is None else out_id
+        N.check(N.lib().nanospec_tree_rerank(_ptr(self.score), _ptr(self.id), self.n, m, _ptr(out_index),
+                                             _ptr(out_id), _stream(dev)), "nanospec_tree_rerank")
+        return out_index, out_id
+
+
+class PackedHead:
+    """The paper's repack design (T6 P:451) as a measured variant:
+    a dense [batch, w_max, d] copy of the active rows kept in slot order.
+    refresh() copies the rows of slots whose id changed (nanospec_repack; run
+    it on a copy stream after the update), head() runs the tensor-core head on
+    the packed rows (nanospec_draft_logits_topk_packed)."""
+
+    def __init__(self, state: ActiveVocab, d_model: int, device):
+        self.state, self.d = state, d_model
+        self.packed = torch.zeros(state.batch, state.w_max, d_model, dtype=torch.bfloat16, device=device)
+        self.tags = torch.full((state.batch, state.w_max), -1, dtype=torch.int32, device=device)
+
+    def refresh(self, seq: int, w_head: torch.Tensor):
+        _need(w_head, torch.bfloat16, "w_head")
+        N.check(N.lib().nanospec_repack(self.state.handle, seq, _ptr(w_head), self.d, w_head.stride(0),
+                                        _ptr(self.packed), self.d, _ptr(self.tags), _stream(w_head.device)),
+                "nanospec_repack")
+
+    def head(self, hidden: torch.Tensor, k: int, out: HeadOutputs):
+        _need(hidden, torch.bfloat16, "hidden")
+        n_nodes = hidden.numel() // (self.state.batch * self.d)
+        _check_out(out, self.state.batch, n_nodes, k, self.state.w_max)
+        N.check(N.lib().nanospec_draft_logits_topk_packed(
+            self.state.handle, _ptr(self.packed), self.d, self.d, _ptr(hidden), n_nodes, k, _ptr(out.topk_logit),
+            _ptr(out.topk_id), _ptr(out.lse), _ptr(out.scratch), out.scratch.numel(), _stream(hidden.device)),
+            "nanospec_draft_logits_topk_packed")
+        return out.topk_logit, out.topk_id, out.lse

@@ -203,3 +203,36 @@ def test_step_with_busy_sms(cuda_ok, llama):
         ids_new, _ = ref.active()
         assert np.array_equal(st.read(0)["ids"], ids_new)
         _check(v[0].cpu().numpy(), i[0].cpu().numpy(), l[0].cpu().numpy(), ids_new, Wb, H, k, f"busy step {s}")
+
+
+def test_repack_variant_matches(cuda_ok, llama):
+    """The paper's repack design as built: after every update the
+    changed slots are re-copied (nanospec_repack) and the head over the packed
+    rows gives bit-identical results to the fused direct gather; the packed
+    rows equal W_head[ids]."""
+    from paper_2605_26444_b200 import ActiveVocab, HeadOutputs, PackedHead, draft_logits_topk
+    W, Wb = llama
+    V, d = W.shape
+    Wm, n, k = 3072, 60, 10
+    zf = SI.Zipf(V)
+    prompt, pre = SI.prompt_and_prefill(zf, 6, 1800, 3)
+    st = ActiveVocab(V, Wm)
+    st.init(0, _t(prompt), _t(pre))
+    ph = PackedHead(st, d, "cuda")
+    o1, o2 = HeadOutputs(1, n, k, Wm, "cuda"), HeadOutputs(1, n, k, Wm, "cuda")
+    copy = torch.cuda.Stream()
+    for s, (dd, vv) in enumerate(SI.decode_steps(zf, 12, 4)):
+        st.update(0, _t(dd), _t(vv))
+        ev = torch.cuda.Event()
+        ev.record()
+        with torch.cuda.stream(copy):  # the paper's copy stream
+            copy.wait_event(ev)
+            ph.refresh(0, W)
+        torch.cuda.current_stream().wait_stream(copy)
+        H = SI.bf16_hidden(n, d, seed=90 + s, device="cuda").reshape(1, n, d)
+        v1, i1, l1, _ = draft_logits_topk(st, W, H, k, out=o1)
+        v2, i2, l2 = ph.head(H, k, o2)
+        torch.cuda.synchronize()
+        assert torch.equal(i1, i2) and torch.equal(v1, v2) and torch.equal(l1, l2), f"step {s}"
+        slots = st.read(0)["slots"]
+        assert torch.equal(ph.packed[0, : len(slots)], W[torch.as_tensor(slots, device="cuda").long()])
