@@ -209,3 +209,18 @@ def test_shards_partition_active_set():
 def test_invalid_ids_dropped_and_flagged():
     s, err = O.stream_init([3, 99, -1, 4], [[5, 77], [5, 6], [1, 2], [0, 0]], 10)
     assert err == 1 and s.tolist() == [3, 4, 5, 6, 1, 2, 0]
+
+
+def test_init_with_k_pre_1():
+    """Eq. 3 with K_pre = 1: S0 = prompt (+) tuple(first-ranked prefill
+    candidate of every position), deduplicated within the union only."""
+    s, err = O.stream_init([10, 11], [[12], [10]], 100)
+    assert err == 0 and list(s) == [10, 11, 12, 10]
+    ids4, _ = O.active_set(s, 100, 4)
+    ids2, _ = O.active_set(s, 100, 2)
+    assert list(ids4) == [10, 11, 12] and list(ids2) == [10, 12]
+    # a repeated candidate inside the union is kept once, its first occurrence
+    s, _ = O.stream_init([5], [[7]], 100)
+    assert list(s) == [5, 7]
+    s, _ = O.stream_init([5, 6, 8], [[7], [7], [9]], 100)
+    assert list(s) == [5, 6, 8, 7, 9]
