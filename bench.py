@@ -248,7 +248,8 @@ def run_ours(args):
     R = max(1, min(R, V // pool))
     W = SI.bf16_weights(V, d, seed=0, device=dev)
     pools = SI.disjoint_pools(V, pool, R, seed=3 + rank)
-    total_steps_per_seq = (args.warmup + 3 * args.steps + 2 * R) // R + 6  # step, two-launch step, update-only, e2e
+    # step, two-launch step, update-only, e2e, repack variant
+    total_steps_per_seq = (args.warmup + 5 * args.steps + 2 * R) // R + 8
     states, outs, upd_d, upd_v = [], [], [], []
     Hs = SI.bf16_hidden(n, d, seed=1 + rank, device=dev, batch=R)
     for r in range(R):
@@ -441,6 +442,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     extra["us_head_packed_rows"] = timed(lambda s: packs[s % R].head(Hs[s % R:s % R + 1], k, outs[s % R]), K)
     snap3 = [st_.workspace.clone() for st_ in states]
+    cursor_save = list(cursor)
 
     def repack_step(s):
         r = s % R
@@ -452,8 +454,9 @@ def run_ours(args):
 
     extra["us_step_repack_variant"] = timed(repack_step, K)
     extra["us_repack_delta_alone"] = timed(lambda s: packs[s % R].refresh(0, W), K)
-    for st_, sn in zip(states, snap3):
+    for st_, sn in zip(states, snap3):  # back to the headline recipe's state and update cursor
         st_.workspace.copy_(sn)
+    cursor[:] = cursor_save
     del snap3, packs
 
     # natural active sets: each of R sequences holds the window of
@@ -706,6 +709,14 @@ def run_dp64(args):
     if world > 1:
         dist.barrier()
     us = _timed_graph(torch, lambda i: step(args.warmup + i), args.steps, stream)
+    # breakdown: the stream kernel alone, and the head (stream + select) without the update
+    from paper_2605_26444_b200 import _native as N
+    brk = {"us_head": round(_timed_graph(torch, lambda i: P.draft_logits_topk(st, W, H, k, impl=args.head, out=out),
+                                         args.steps, stream), 3)}
+    N.check(N.lib().nanospec_debug_set_head_mode(1), "head mode")
+    brk["us_stream_kernel_alone"] = round(_timed_graph(
+        torch, lambda i: P.draft_logits_topk(st, W, H, k, impl=args.head, out=out), args.steps, stream), 3)
+    N.check(N.lib().nanospec_debug_set_head_mode(-1), "head mode")
     if world > 1:
         t = torch.tensor([us], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -721,7 +732,7 @@ def run_dp64(args):
             "roofline": {"bound": "hbm", "achieved": round(gbps, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(gbps / peak, 4), "traffic": None, "peak_source": peak_src,
                          "kernel": "update_batch + batched draft_logits_topk, per rank"},
-            "gpu_launches": 3 * args.steps}
+            "breakdown": brk, "gpu_launches": 3 * args.steps}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

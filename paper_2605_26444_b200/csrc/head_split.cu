@@ -476,8 +476,7 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
 // lists anywhere.
 constexpr int kBThreads = 1024;
 constexpr int kBWarps = kBThreads / 32;
-constexpr int kRoundTiles = kBWarps;              // 32 tiles per round
-constexpr int kCand = kMaxK + kRoundTiles * kBM;  // worst case: every row of a round ties at T
+constexpr int kSmallBin = 96;                     // candidates a one-pass threshold may leave
 
 // One warp, a 256-bin histogram: the largest bin b whose suffix count
 // (bins >= b) reaches `need`, and how many keys are still needed inside it:
@@ -511,37 +510,67 @@ __device__ __forceinline__ uint2 radix_bin(const uint32_t* hist, uint32_t need) 
   return make_uint2(bin, rem);
 }
 
+// NP (sequence, node) pairs per CTA, WP = 32 / NP warps each, TPW tiles per
+// warp per round: <1, 1> for few pairs (the headline: 60 CTAs of one pair,
+// 32 tiles a round), <4, 3> for many pairs whose tiles fit one round (dp64:
+// 24 tiles per sequence, 3840 pairs -> 960 CTAs).  The pairs of a CTA run in
+// lock step (the CTA's barriers); each pair has its own shared-memory slice.
+template <int NP, int TPW>
+struct BCfg {
+  static constexpr int WP = kBWarps / NP;               // warps per pair
+  static constexpr int kRound = WP * TPW;               // tiles per round
+  static constexpr int kCandN = kMaxK + kRound * kBM;   // worst case: every row of a round ties at T
+  static constexpr size_t kSmem = (size_t)NP * kCandN * 8;  // dynamic: the candidate arrays
+};
+
+template <int NP, int TPW>
 __global__ void __launch_bounds__(kBThreads, 1) head_select_kernel(const __grid_constant__ SplitArgs a) {
-  __shared__ uint2 cand[kCand];  // [0, k): the running top-k (sorted); then the round's candidates
-  __shared__ uint2 res[kMaxK];
-  __shared__ uint32_t hist1[256], hist2[256];
-  __shared__ uint32_t sh_wm[kBWarps];
-  __shared__ float sh_es[kBWarps];
-  __shared__ uint32_t sh_b1, sh_need, sh_T;
-  __shared__ int sh_cnt;
-  __shared__ float sh_M, sh_E;  // running lse: maximum and sum exp(z - maximum)
+  using C = BCfg<NP, TPW>;
+  constexpr int WP = C::WP;
+  extern __shared__ __align__(16) uint8_t bsm[];
+  __shared__ uint2 res_all[NP][kMaxK];
+  __shared__ uint32_t hist1_all[NP][256], hist2_all[NP][256];
+  __shared__ uint32_t sh_wm_all[NP][WP];
+  __shared__ float sh_es_all[NP][WP];
+  __shared__ uint32_t sh_b1_all[NP], sh_need_all[NP], sh_T_all[NP];
+  __shared__ int sh_cnt_all[NP];
+  __shared__ float sh_M_all[NP], sh_E_all[NP];  // running lse: maximum and sum exp(z - maximum)
   const HeadProblem& p = a.p;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int pi = warp / WP, wq = warp - pi * WP, ptid = tid - pi * WP * 32;  // pair of the CTA, warp / thread in it
+  uint2* cand = reinterpret_cast<uint2*>(bsm) + (size_t)pi * C::kCandN;  // [0, k): running top-k; then candidates
+  uint2* res = res_all[pi];
+  uint32_t* hist1 = hist1_all[pi];
+  uint32_t* hist2 = hist2_all[pi];
+  uint32_t* sh_wm = sh_wm_all[pi];
+  float* sh_es = sh_es_all[pi];
   const int k = a.k;
-  const int seq = blockIdx.x / p.n, node = blockIdx.x - seq * p.n;
+  const int pair = blockIdx.x * NP + pi;
+  const bool live_pair = pair < p.batch * p.n;
+  const int seq = live_pair ? pair / p.n : 0, node = live_pair ? pair - seq * p.n : 0;
   const int ntp = a.tps + a.n_patch;
   const long long pst = (long long)p.n * kBM;
   const int r0 = 4 * lane;
   warm_params(a);
-  if (tid < kMaxK) cand[tid] = make_uint2(0u, 0xffffffffu);
-  if (tid < 256) { hist1[tid] = 0u; hist2[tid] = 0u; }
-  if (tid == 0) { sh_cnt = 0; sh_M = -INFINITY; sh_E = 0.f; }
+  if (ptid < kMaxK) cand[ptid] = make_uint2(0u, 0xffffffffu);
+  if (ptid < 256) { hist1[ptid] = 0u; hist2[ptid] = 0u; }
+  if (ptid == 0) { sh_cnt_all[pi] = 0; sh_M_all[pi] = -INFINITY; sh_E_all[pi] = 0.f; }
   if (tid == 0) trace_b(a, 0);
-  if (lane == 0 && warp < ntp) {  // warm the translations / L2 lines of round 0 while A still runs
-    int S0, b0;
-    tile_units(a, global_tile(a, seq, warp), S0, b0);
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.rowgid + ((long long)seq * ntp + warp) * kBM));
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.part + (long long)b0 * pst + (long long)node * kBM));
-  }
   // round 0's addresses (index math only) before the wait
-  int S = 0, base = 0;
-  bool on = warp < ntp;
-  if (on) tile_units(a, global_tile(a, seq, warp), S, base);
+  int S[TPW], base[TPW];
+  bool on[TPW];
+#pragma unroll
+  for (int j = 0; j < TPW; ++j) {
+    const int tile = wq * TPW + j;
+    on[j] = live_pair && tile < ntp;
+    S[j] = 0;
+    base[j] = 0;
+    if (on[j]) tile_units(a, global_tile(a, seq, tile), S[j], base[j]);
+    if (on[j] && lane == 0) {  // warm the translations / L2 lines while A still runs
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.rowgid + ((long long)seq * ntp + tile) * kBM));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.part + (long long)base[j] * pst + (long long)node * kBM));
+    }
+  }
   pdl_wait();  // A complete: partials, row ids (and the fused step's drop bitmap) visible
   asm volatile("griddepcontrol.launch_dependents;");
   if (tid == 0) trace_b(a, 1);
@@ -549,109 +578,140 @@ __global__ void __launch_bounds__(kBThreads, 1) head_select_kernel(const __grid_
     p.trace[(long long)(a.trace_base + blockIdx.x) * kTraceSlots + 14] = clock64();
     p.trace[(long long)(a.trace_base + blockIdx.x) * kTraceSlots + 12] = 0xB;  // a B row
   }
-  const int mrow = __ldcg(a.mrows + seq);  // regular tiles past it hold no rows (skipped after round 0)
-  for (int v0 = 0; v0 < ntp; v0 += kRoundTiles) {
-    const int treg = (mrow + kBM - 1) / kBM;
-    if (v0 > 0 && v0 >= treg && v0 + kRoundTiles <= a.tps) continue;  // a chunk of tiles past n_active
-    const int tile = v0 + warp;  // regular tiles [0, tps), then patch tiles
-    if (v0 > 0) {
-      on = tile < ntp && !(tile >= treg && tile < a.tps);
-      S = 0;
-      base = 0;
-      if (on) tile_units(a, global_tile(a, seq, tile), S, base);
-    }
-    const int4 g4 = on ? __ldcg(reinterpret_cast<const int4*>(a.rowgid + ((long long)seq * ntp + tile) * kBM) + lane)
-                       : make_int4(-1, -1, -1, -1);
-    const uint32_t dw = (on && a.drop) ? __ldcg(&a.drop[tile * 4 + (lane >> 3)]) >> ((lane & 7) * 4) : 0u;
-    float z[4] = {0.f, 0.f, 0.f, 0.f};
-    {
-      const float* src = a.part + (long long)base * pst + (long long)node * kBM + r0;
-      const int rot = S ? tile % S : 0;
-      for (int c0 = 0; c0 < S; c0 += 8) {  // K chunk c was computed by split (c - tile) mod S
-        float4 x[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (c0 + q < S) {
-            int sp = c0 + q - rot;
-            if (sp < 0) sp += S;
-            x[q] = __ldcg(reinterpret_cast<const float4*>(src + (long long)sp * pst));
-          }
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (c0 + q < S) { z[0] += x[q].x; z[1] += x[q].y; z[2] += x[q].z; z[3] += x[q].w; }
-      }
-    }
-    if (tid == 0 && v0 == 0) trace_b(a, 5);
-    uint32_t key[4], gid[4];
+  int treg = a.tps;  // regular tiles holding rows (known after round 0; NP == 1 only: one round otherwise)
+  for (int v0 = 0; v0 < ntp; v0 += C::kRound) {
+    if (v0 > 0 && v0 >= treg && v0 + C::kRound <= a.tps) continue;  // a chunk of tiles past n_active
+    uint32_t key[4 * TPW], gid[4 * TPW];  // the logit is key_value(key): no float copy kept
     uint32_t lm = 0u;
-    {
+#pragma unroll
+    for (int j = 0; j < TPW; ++j) {
+      const int tile = v0 + wq * TPW + j;  // regular tiles [0, tps), then patch tiles
+      if (v0 > 0) {
+        on[j] = live_pair && tile < ntp && !(tile >= treg && tile < a.tps);
+        S[j] = 0;
+        base[j] = 0;
+        if (on[j]) tile_units(a, global_tile(a, seq, tile), S[j], base[j]);
+      }
+      const int4 g4 = on[j] ? __ldcg(reinterpret_cast<const int4*>(a.rowgid + ((long long)seq * ntp + tile) * kBM) + lane)
+                            : make_int4(-1, -1, -1, -1);
+      const uint32_t dw = (on[j] && a.drop) ? __ldcg(&a.drop[tile * 4 + (lane >> 3)]) >> ((lane & 7) * 4) : 0u;
+      float zz[4] = {0.f, 0.f, 0.f, 0.f};
+      if (TPW > 1) {  // the many-pair layout runs with split-K 1: one partial per tile
+        if (on[j] && S[j] == 1) {
+          const float4 x = __ldcg(reinterpret_cast<const float4*>(a.part + (long long)base[j] * pst +
+                                                                   (long long)node * kBM + r0));
+          zz[0] = x.x; zz[1] = x.y; zz[2] = x.z; zz[3] = x.w;
+        }
+      } else {
+        const float* src = a.part + (long long)base[j] * pst + (long long)node * kBM + r0;
+        const int Sj = S[j], rot = Sj ? tile % Sj : 0;
+        for (int c0 = 0; c0 < Sj; c0 += 8) {  // K chunk c was computed by split (c - tile) mod S
+          float4 x[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (c0 + q < Sj) {
+              int sp = c0 + q - rot;
+              if (sp < 0) sp += Sj;
+              x[q] = __ldcg(reinterpret_cast<const float4*>(src + (long long)sp * pst));
+            }
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (c0 + q < Sj) { zz[0] += x[q].x; zz[1] += x[q].y; zz[2] += x[q].z; zz[3] += x[q].w; }
+        }
+      }
       const int32_t g[4] = {g4.x, g4.y, g4.z, g4.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const bool ok = g[i] >= 0 && !((dw >> i) & 1u);
-        key[i] = ok ? float_key(z[i]) : 0u;
-        gid[i] = ok ? (uint32_t)g[i] : 0xffffffffu;
-        lm = key[i] > lm ? key[i] : lm;
+        key[4 * j + i] = ok ? float_key(zz[i]) : 0u;
+        gid[4 * j + i] = ok ? (uint32_t)g[i] : 0xffffffffu;
+        lm = key[4 * j + i] > lm ? key[4 * j + i] : lm;
         if (g[i] >= 0 && p.logits) {
           const long long col = tile < a.tps ? (long long)tile * kBM + r0 + i
                                              : (long long)p.max_ids + (tile - a.tps) * kBM + r0 + i;
-          p.logits[((long long)seq * p.n + node) * a.dbg_ld + col] = z[i];
+          p.logits[((long long)seq * p.n + node) * a.dbg_ld + col] = zz[i];
         }
       }
     }
+    if (tid == 0 && v0 == 0) trace_b(a, 5);
     // ---- pass 1 of the radix select: histogram of the keys' top 8 bits
     const uint32_t wm = __reduce_max_sync(0xffffffffu, lm);
-    if (lane == 0) sh_wm[warp] = wm;
+    if (lane == 0) sh_wm[wq] = wm;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 4 * TPW; ++i)
       if (key[i]) atomicAdd(&hist1[key[i] >> 24], 1u);
     if (tid == 0 && v0 == 0) trace_b(a, 6);
     __syncthreads();  // S1: histogram 1, warp maxima; the running top-k of the previous round
     if (tid == 0 && v0 == 0) trace_b(a, 2);
-    const uint32_t Mk = __reduce_max_sync(0xffffffffu, sh_wm[lane]);  // the round's maximum key
+    if (NP == 1 && v0 == 0) treg = (__ldcg(a.mrows + seq) + kBM - 1) / kBM;
+    const uint32_t Mk = __reduce_max_sync(0xffffffffu, lane < WP ? sh_wm[lane] : 0u);  // the round's maximum key
     const float M = key_value(Mk);
     {  // lse partial of the round (one exp per row against the round maximum)
       float es = 0.f;
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (key[i]) es += __expf(z[i] - M);
+      for (int i = 0; i < 4 * TPW; ++i)
+        if (key[i]) es += __expf(key_value(key[i]) - M);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
-      if (lane == 0) sh_es[warp] = es;
+      if (lane == 0) sh_es[wq] = es;
     }
-    if (warp == 0) {
+    if (wq == 0) {
+      // bin of the round's k-th largest key (top 8 bits) and the keys still
+      // needed inside it; when that bin and the ones above hold few keys the
+      // threshold is its lower edge and the second pass is skipped
       const uint2 r = radix_bin(hist1, k);
-      if (lane == 0) { sh_b1 = r.x; sh_need = r.y; }
-    }
-    __syncthreads();  // S2: bin of the k-th largest key (top 8 bits), keys still needed inside it
-    const uint32_t b1 = sh_b1;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (key[i] && (key[i] >> 24) == b1) atomicAdd(&hist2[(key[i] >> 16) & 0xffu], 1u);
-    __syncthreads();  // S3: histogram 2
-    if (warp == 0) {
-      // T = the 16-bit prefix of the round's k-th largest key (0: fewer than k
-      // keys); at least k round keys are >= T, so no round key below
-      // max(T, running k-th key) is in the top-k of (running list U round)
-      const uint2 r = radix_bin(hist2, sh_need);
-      const uint32_t T = b1 == 0xffffffffu ? 0u : (r.x == 0xffffffffu ? (b1 << 24) : (b1 << 24) | (r.x << 16));
       const uint32_t Tk = cand[k - 1].x;
-      if (lane == 0) sh_T = T > Tk ? T : Tk;
+      if (lane == 0) {
+        sh_b1_all[pi] = r.x;
+        sh_need_all[pi] = r.y;
+        uint32_t T = 0xffffffffu;  // "second pass needed"
+        if (r.x == 0xffffffffu) T = 0u;  // fewer than k keys: all of them are candidates
+        else if ((uint32_t)k - r.y + hist1[r.x] <= (uint32_t)kSmallBin) T = r.x << 24;
+        sh_T_all[pi] = T == 0xffffffffu ? T : (T > Tk ? T : Tk);
+      }
+      __syncwarp();
 #pragma unroll
-      for (int j = 0; j < 8; ++j) hist1[8 * lane + j] = 0u;  // ready for the next round
-    } else if (warp == kBWarps - 1) {  // fold the round's lse into the running one
-      float x = sh_es[lane];
+      for (int j = 0; j < 8; ++j) hist1[8 * lane + j] = 0u;  // ready for the next round (read above)
+    }
+    if (ptid < k) res[ptid] = make_uint2(0u, 0xffffffffu);  // fewer than k candidates: padding
+    __syncthreads();  // S2: threshold or pass-2 bin; every warp's lse partial
+    if (wq == WP - 1) {  // fold the round's lse into the running one
+      float x = lane < WP ? sh_es[lane] : 0.f;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-      if (lane == 0 && Mk != 0u) lse_fold(sh_M, sh_E, M, x);
+      if (lane == 0 && Mk != 0u) lse_fold(sh_M_all[pi], sh_E_all[pi], M, x);
     }
-    if (tid < k) res[tid] = make_uint2(0u, 0xffffffffu);  // fewer than k candidates: padding
-    __syncthreads();  // S4: threshold
-    const uint32_t T = sh_T;
+    bool need2 = false;  // pass 2 for any pair of the CTA: its barriers are the CTA's
+#pragma unroll
+    for (int q = 0; q < NP; ++q) need2 = need2 || sh_T_all[q] == 0xffffffffu;
+    if (need2) {  // pass 2: the next 8 bits of the keys inside bin b1
+      const uint32_t b1 = sh_b1_all[pi];
+      const bool mine2 = sh_T_all[pi] == 0xffffffffu;
+      if (mine2) {
+#pragma unroll
+        for (int i = 0; i < 4 * TPW; ++i)
+          if (key[i] && (key[i] >> 24) == b1) atomicAdd(&hist2[(key[i] >> 16) & 0xffu], 1u);
+      }
+      __syncthreads();  // S3: histogram 2
+      if (wq == 0 && mine2) {
+        // T = the 16-bit prefix of the round's k-th largest key: at least k round
+        // keys are >= T, so no round key below max(T, running k-th key) is in
+        // the top-k of (running list U round)
+        const uint2 r = radix_bin(hist2, sh_need_all[pi]);
+        const uint32_t T = r.x == 0xffffffffu ? (b1 << 24) : (b1 << 24) | (r.x << 16);
+        const uint32_t Tk = cand[k - 1].x;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) hist2[8 * lane + j] = 0u;  // ready for the next round (read above)
+        __syncwarp();
+        if (lane == 0) sh_T_all[pi] = T > Tk ? T : Tk;
+      }
+      __syncthreads();  // S4: threshold
+    }
+    const uint32_t T = sh_T_all[pi];
     // ---- the keys >= T go behind the running top-k
     int c = 0;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) c += (key[i] != 0u && key[i] >= T) ? 1 : 0;
+    for (int i = 0; i < 4 * TPW; ++i) c += (key[i] != 0u && key[i] >= T) ? 1 : 0;
     if (__ballot_sync(0xffffffffu, c > 0)) {
       int pre = c;
 #pragma unroll
@@ -660,17 +720,17 @@ __global__ void __launch_bounds__(kBThreads, 1) head_select_kernel(const __grid_
         if (lane >= o) pre += y;
       }
       int wbase = 0;
-      if (lane == 31) wbase = atomicAdd(&sh_cnt, pre);
+      if (lane == 31) wbase = atomicAdd(&sh_cnt_all[pi], pre);
       wbase = __shfl_sync(0xffffffffu, wbase, 31);
       int o2 = k + wbase + pre - c;
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 4 * TPW; ++i)
         if (key[i] != 0u && key[i] >= T) cand[o2++] = make_uint2(key[i], gid[i]);
     }
     __syncthreads();  // S5: candidates in place
     if (tid == 0 && v0 == 0) trace_b(a, 7);
-    const int tot = k + sh_cnt;
-    for (int e = tid; e < tot; e += kBThreads) {  // every candidate ranked by its own thread
+    const int tot = k + sh_cnt_all[pi];
+    for (int e = ptid; e < tot; e += WP * 32) {  // every candidate ranked by its own thread
       const uint2 me = cand[e];
       if (me.x == 0u) continue;
       int rk = 0;
@@ -681,22 +741,22 @@ __global__ void __launch_bounds__(kBThreads, 1) head_select_kernel(const __grid_
       }
       if (rk < k) res[rk] = me;
     }
-    if (tid < 256) hist2[tid] = 0u;
     __syncthreads();  // S6: the round's top-k in res
     if (tid == 0 && v0 == 0) trace_b(a, 9);
-    if (tid < k) cand[tid] = res[tid];  // the new running top-k
-    if (tid == 0) sh_cnt = 0;
+    if (ptid < k) cand[ptid] = res[ptid];  // the new running top-k
+    if (ptid == 0) sh_cnt_all[pi] = 0;
   }
-  if (warp != 0) return;
+  if (wq != 0 || !live_pair) return;
   const long long ob = ((long long)seq * p.n + node) * k;
   if (lane < k) {
     const uint2 r = res[lane];
     a.topk_logit[ob + lane] = r.x ? key_value(r.x) : -INFINITY;
     a.topk_id[ob + lane] = r.x ? (int32_t)r.y : -1;
   }
-  if (a.lse && lane == 0) a.lse[(long long)seq * p.n + node] = sh_M == -INFINITY ? -INFINITY : sh_M + logf(sh_E);
-  if (lane == 0) trace_b(a, 4);
-  if (lane == 0 && p.trace) p.trace[(long long)(a.trace_base + blockIdx.x) * kTraceSlots + 15] = clock64();
+  if (a.lse && lane == 0)
+    a.lse[(long long)seq * p.n + node] = sh_M_all[pi] == -INFINITY ? -INFINITY : sh_M_all[pi] + logf(sh_E_all[pi]);
+  if (tid == 0) trace_b(a, 4);
+  if (tid == 0 && p.trace) p.trace[(long long)(a.trace_base + blockIdx.x) * kTraceSlots + 15] = clock64();
 }
 
 // ------------------------------------------------------------------ host side
@@ -722,6 +782,8 @@ SplitLayout split_layout(int batch, int max_ids, int n, int num_sms) {
 }
 
 int g_split_pdl = 1;
+int g_num_sms = 148;  // set by the launchers (the select kernel's layout choice)
+int num_sms_cached() { return g_num_sms; }
 int g_stream_only = 0;  // debug mode 1: kernel A alone (measurement; no outputs are written)
 // experiments (NANOSPEC_SPLIT_FLAGS): 1 = skip kernel B, 2 = no PDL, 4 = kernel B twice,
 // 8 = W rows with an L2 evict-first policy, 16 = kernel B alone
@@ -780,6 +842,32 @@ cudaError_t set_attr_once() {
   return e;
 }
 
+template <int NP, int TPW>
+cudaError_t launch_select_cfg(const SplitArgs& b, cudaStream_t stream) {
+  using C = BCfg<NP, TPW>;
+  static bool done[64] = {false};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (!done[dev]) {
+    const cudaError_t e = cudaFuncSetAttribute(head_select_kernel<NP, TPW>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
+    if (e != cudaSuccess) return e;
+    done[dev] = true;
+  }
+  const int pairs = b.p.batch * b.p.n;
+  return launch_ex(head_select_kernel<NP, TPW>, dim3((pairs + NP - 1) / NP), kBThreads, C::kSmem, stream, b);
+}
+
+// Many (sequence, node) pairs whose tiles fit one round of the 4-pair layout
+// (dp64: 24 tiles, 3840 pairs): four pairs per CTA; else one pair per CTA.
+cudaError_t launch_select(const SplitArgs& b, int num_sms, cudaStream_t stream) {
+  const int pairs = b.p.batch * b.p.n;
+  const int ntp = b.tps + b.n_patch;
+  if (pairs >= 4 * num_sms && ntp <= BCfg<4, 3>::kRound && b.S == 1 && b.extra == 0)
+    return launch_select_cfg<4, 3>(b, stream);
+  return launch_select_cfg<1, 1>(b, stream);
+}
+
 template <int NT, bool FUSED>
 cudaError_t launch_pair_of_kernels(const SplitArgs& a, int grid_a, cudaStream_t stream) {
   cudaError_t e = set_attr_once<NT, FUSED>();
@@ -790,9 +878,7 @@ cudaError_t launch_pair_of_kernels(const SplitArgs& a, int grid_a, cudaStream_t 
     e = launch_ex(head_stream_kernel<NT, FUSED>, dim3(grid_a), kAThreads, ACfg<NT>::kSmemBytes, stream, a);
     if (e != cudaSuccess || (split_flags() & 1) || g_stream_only) return e;
   }
-  e = launch_ex(head_select_kernel, dim3(a.p.batch * a.p.n), kBThreads, 0, stream, b);
-  if (e != cudaSuccess || !(split_flags() & 4)) return e;
-  return launch_ex(head_select_kernel, dim3(a.p.batch * a.p.n), kBThreads, 0, stream, b);  // experiment
+  return launch_select(b, num_sms_cached(), stream);
 }
 
 template <bool FUSED>
@@ -855,6 +941,7 @@ void plan_splits(SplitArgs& a, int U, int KB) {
 cudaError_t launch_head_tc(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse,
                            void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t stream) {
   if (!shape_ok(p, k)) return cudaErrorNotSupported;
+  g_num_sms = num_sms;
   const int G = num_sms < 256 ? num_sms : 256;
   const SplitLayout L = split_layout(p.batch, p.max_ids, p.n, 256);
   if (L.total > scratch_bytes) return cudaErrorInvalidValue;

@@ -121,7 +121,7 @@ if args.trace:
                 cyc = rows_[ok, 15] - rows_[ok, 14]
                 ns = rows_[ok, 9 if nm == "A" else 4] - rows_[ok, 0 if nm == "A" else 1]
                 print(f"    {nm} SM clock ~{np.median(cyc / np.maximum(ns, 1)) * 1e3:.0f} MHz")
-        for name, e in (("B start", 0), ("B dep", 1), ("B loaded", 5), ("B hist1", 6), ("B S1", 2), ("B S5", 7), ("B S6", 9), ("B tiles", 3), ("B done", 4)):
+        for name, e in (("B start", 0), ("B dep", 1), ("B loaded", 5), ("B hist1", 6), ("B S1", 2), ("B cands", 7), ("B ranked", 9), ("B tiles", 3), ("B done", 4)):
             c = t[nA:nA + 512, e]
             c = c[c > 0]
             if len(c):
