@@ -60,10 +60,12 @@ constexpr int kMaxS = 32;          // K splits per tile
 constexpr int kMaxK = 32;
 constexpr long long kSpin = 1ll << 30;  // updater's arrival poll bound (a trap beats a hung GPU)
 
-template <int NT>
+template <int NT, int AG = 1>  // AG: 64-column K atoms per pipeline stage
 struct ACfg {
-  static constexpr int kABytes = kBM * kBK * 2;   // 16 KB of W rows
-  static constexpr int kBBytes = NT * kBK * 2;    // NT x 128 B of H
+  static constexpr int kAtomA = kBM * kBK * 2;    // 16 KB of W rows per atom
+  static constexpr int kAtomB = NT * kBK * 2;     // NT x 128 B of H per atom
+  static constexpr int kABytes = AG * kAtomA;
+  static constexpr int kBBytes = AG * kAtomB;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStages = (kBudget / kStageBytes) > 8 ? 8 : (kBudget / kStageBytes);
   static constexpr int kTmemCols = NT < 32 ? 32 : NT;
@@ -95,7 +97,6 @@ struct SplitArgs {
   int k;
   long long dbg_ld;     // debug logits: floats between the rows of one (sequence, node)
   int trace_base;       // debug trace: B's CTA b writes trace row trace_base + b (after A's rows)
-  int w_evict_first;    // W rows streamed with an L2 evict-first policy
 };
 
 // The kernel parameters live in the constant bank; their first reads miss the
@@ -219,9 +220,9 @@ struct SplitPublish {
 };
 
 // ------------------------------------------------------------------ kernel A
-template <int NT, bool FUSED>
+template <int NT, bool FUSED, int AG>
 __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_constant__ SplitArgs a) {
-  using C = ACfg<NT>;
+  using C = ACfg<NT, AG>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStageArea);
@@ -343,6 +344,7 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
         continue;
       }
       const int kb0 = un.kb0, nk = un.nk;
+      const int nst = (nk + AG - 1) / AG;  // pipeline stages of this unit
       if (warp < kLW) {
         // ---------------- loaders: rows of W_head + H into SW128 stages
         const uint16_t* rp[2];
@@ -356,33 +358,39 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
           rp[i] = g >= 0 ? base + (tid & 7) * 8 : nullptr;
         }
         const uint16_t* hp = p.h + (long long)un.seq * p.n * p.d + (tid & 7) * 8;
-        uint64_t pol = 0;
-        if (a.w_evict_first) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
         if (tid == 0 && local == 0) trace_mark(p.trace, 2);
         if (tid == 0 && local == 0 && p.trace) p.trace[(long long)blockIdx.x * kTraceSlots + 13] = clock64();
-        for (int q = 0; q < nk + C::kStages - 1; ++q) {
-          if (q < nk) {
+        for (int q = 0; q < nst + C::kStages - 1; ++q) {
+          if (q < nst) {
             const int g_it = it + q;
             const int stage = g_it % C::kStages;
             if (g_it >= C::kStages) mbar_wait(smem_u32(&bars[C::kStages + stage]), ((g_it / C::kStages) - 1) & 1);
             const uint32_t sA = smem_u32(smem + stage * C::kStageBytes);
             const uint32_t sB = sA + C::kABytes;
-            const int kcol = (kb0 + q) * kBK;
+            // a row's AG atoms back to back: AG * 128 contiguous bytes per row per stage
 #pragma unroll
-            for (int i = 0; i < 2; ++i) {
-              if (a.w_evict_first)
-                cp_async16_hint(sA + (lr + 64 * i) * 128 + swz, rp[i] ? (const void*)(rp[i] + kcol) : (const void*)p.w,
-                                rp[i] ? 16u : 0u, pol);
-              else
-                cp_async16(sA + (lr + 64 * i) * 128 + swz, rp[i] ? (const void*)(rp[i] + kcol) : (const void*)p.w,
-                           rp[i] ? 16u : 0u);
-            }
+            for (int i = 0; i < 2; ++i)
 #pragma unroll
-            for (int i = 0; i < (NT * 8 + kLoaders - 1) / kLoaders; ++i) {
-              const int hr = lr + 64 * i;
-              if (hr < NT)
-                cp_async16(sB + hr * 128 + swz, hr < p.n ? (const void*)(hp + (long long)hr * p.d + kcol) : (const void*)p.h,
-                           hr < p.n ? 16u : 0u);
+              for (int at = 0; at < AG; ++at) {
+                const bool in = q * AG + at < nk;
+                const int kcol = (kb0 + q * AG + at) * kBK;
+                if (in)
+                  cp_async16(sA + at * C::kAtomA + (lr + 64 * i) * 128 + swz,
+                             rp[i] ? (const void*)(rp[i] + kcol) : (const void*)p.w, rp[i] ? 16u : 0u);
+              }
+#pragma unroll
+            for (int at = 0; at < AG; ++at) {
+              const int kcol = (kb0 + q * AG + at) * kBK;
+              if (q * AG + at < nk) {
+#pragma unroll
+                for (int i = 0; i < (NT * 8 + kLoaders - 1) / kLoaders; ++i) {
+                  const int hr = lr + 64 * i;
+                  if (hr < NT)
+                    cp_async16(sB + at * C::kAtomB + hr * 128 + swz,
+                               hr < p.n ? (const void*)(hp + (long long)hr * p.d + kcol) : (const void*)p.h,
+                               hr < p.n ? 16u : 0u);
+                }
+              }
             }
           }
           cp_async_commit();
@@ -421,7 +429,7 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
           mbar_wait(smem_u32(&bars[2 * C::kStages + 1]), (nrun - 1) & 1);
           tc_fence_after();
         }
-        for (int q = 0; q < nk; ++q) {
+        for (int q = 0; q < nst; ++q) {
           const int g_it = it + q;
           const int stage = g_it % C::kStages;
           mbar_wait(smem_u32(&bars[stage]), (g_it / C::kStages) & 1);
@@ -430,15 +438,20 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
             const uint32_t sA = smem_u32(smem + stage * C::kStageBytes);
             const uint32_t sB = sA + C::kABytes;
 #pragma unroll
-            for (int kk = 0; kk < kBK / 16; ++kk)
-              umma_bf16(tmem, sw128_desc(sA + kk * 32), sw128_desc(sB + kk * 32), idesc, (q | kk) ? 1u : 0u);
+            for (int at = 0; at < AG; ++at)
+              if (q * AG + at < nk) {
+#pragma unroll
+                for (int kk = 0; kk < kBK / 16; ++kk)
+                  umma_bf16(tmem, sw128_desc(sA + at * C::kAtomA + kk * 32), sw128_desc(sB + at * C::kAtomB + kk * 32),
+                            idesc, (q | at | kk) ? 1u : 0u);
+              }
             umma_commit(smem_u32(&bars[C::kStages + stage]));
-            if (q == nk - 1) umma_commit(smem_u32(&bars[2 * C::kStages]));
+            if (q == nst - 1) umma_commit(smem_u32(&bars[2 * C::kStages]));
           }
           __syncwarp();
         }
       }
-      it += nk;
+      it += nst;
       ++nrun;
       if (nx) {
         if (tid < kBM) ids_s[buf ^ 1][tid] = nx_id;
@@ -523,7 +536,7 @@ struct BCfg {
   static constexpr size_t kSmem = (size_t)NP * kCandN * 8;  // dynamic: the candidate arrays
 };
 
-template <int NP, int TPW>
+template <int NP, int TPW, bool MR>  // MR: several rounds (the later ones may skip the radix passes)
 __global__ void __launch_bounds__(kBThreads, 1) head_select_kernel(const __grid_constant__ SplitArgs a) {
   using C = BCfg<NP, TPW>;
   constexpr int WP = C::WP;
@@ -634,9 +647,70 @@ __global__ void __launch_bounds__(kBThreads, 1) head_select_kernel(const __grid_
       }
     }
     if (tid == 0 && v0 == 0) trace_b(a, 5);
-    // ---- pass 1 of the radix select: histogram of the keys' top 8 bits
     const uint32_t wm = __reduce_max_sync(0xffffffffu, lm);
     if (lane == 0) sh_wm[wq] = wm;
+    if (MR && NP == 1 && v0 > 0) {
+      // ---- a later round: when the top-k so far already prunes all but a few
+      // keys (<= 4 keys on each of <= 32 threads), its k-th key is the
+      // threshold and the radix passes are skipped
+      const uint32_t Tk = res[k - 1].x;  // the top-k so far (stable since the previous round's last barrier)
+      int q = 0;
+#pragma unroll
+      for (int i = 0; i < 4 * TPW; ++i) q |= (key[i] != 0u && key[i] >= Tk) ? 1 : 0;
+      if (__syncthreads_count(q) <= 32) {  // also publishes the warp maxima
+        const uint32_t Mk = __reduce_max_sync(0xffffffffu, lane < WP ? sh_wm[lane] : 0u);
+        const float M = key_value(Mk);
+        float es = 0.f;
+#pragma unroll
+        for (int i = 0; i < 4 * TPW; ++i)
+          if (key[i]) es += __expf(key_value(key[i]) - M);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
+        if (lane == 0) sh_es[wq] = es;
+        if (ptid < k) res[ptid] = make_uint2(0u, 0xffffffffu);
+        int c = 0;
+#pragma unroll
+        for (int i = 0; i < 4 * TPW; ++i) c += (key[i] != 0u && key[i] >= Tk) ? 1 : 0;
+        if (__ballot_sync(0xffffffffu, c > 0)) {
+          int pre = c;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, pre, o);
+            if (lane >= o) pre += y;
+          }
+          int wbase = 0;
+          if (lane == 31) wbase = atomicAdd(&sh_cnt_all[pi], pre);
+          wbase = __shfl_sync(0xffffffffu, wbase, 31);
+          int o2 = k + wbase + pre - c;
+#pragma unroll
+          for (int i = 0; i < 4 * TPW; ++i)
+            if (key[i] != 0u && key[i] >= Tk) cand[o2++] = make_uint2(key[i], gid[i]);
+        }
+        __syncthreads();  // candidates, lse partials
+        if (wq == WP - 1) {
+          float x = lane < WP ? sh_es[lane] : 0.f;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+          if (lane == 0 && Mk != 0u) lse_fold(sh_M_all[pi], sh_E_all[pi], M, x);
+        }
+        const int tot = k + sh_cnt_all[pi];
+        for (int e = ptid; e < tot; e += WP * 32) {
+          const uint2 me = cand[e];
+          if (me.x == 0u) continue;
+          int rk = 0;
+          for (int f = 0; f < tot; ++f) {
+            const uint2 o = cand[f];
+            rk += (o.x != 0u && key_before(o.x, o.y, me.x, me.y)) ? 1 : 0;
+          }
+          if (rk < k) res[rk] = me;
+        }
+        __syncthreads();  // the round's top-k in res
+        if (ptid < k) cand[ptid] = res[ptid];
+        if (ptid == 0) sh_cnt_all[pi] = 0;
+        continue;
+      }
+    }
+    // ---- pass 1 of the radix select: histogram of the keys' top 8 bits
 #pragma unroll
     for (int i = 0; i < 4 * TPW; ++i)
       if (key[i]) atomicAdd(&hist1[key[i] >> 24], 1u);
@@ -785,8 +859,8 @@ int g_split_pdl = 1;
 int g_num_sms = 148;  // set by the launchers (the select kernel's layout choice)
 int num_sms_cached() { return g_num_sms; }
 int g_stream_only = 0;  // debug mode 1: kernel A alone (measurement; no outputs are written)
-// experiments (NANOSPEC_SPLIT_FLAGS): 1 = skip kernel B, 2 = no PDL, 4 = kernel B twice,
-// 8 = W rows with an L2 evict-first policy, 16 = kernel B alone
+// experiments (NANOSPEC_SPLIT_FLAGS): 1 = skip kernel B, 2 = no PDL, 16 = kernel B alone,
+// 32 = one K atom per pipeline stage
 int g_split_flags = -1;
 int split_flags() {
   if (g_split_flags < 0) {
@@ -830,32 +904,32 @@ cudaError_t launch_ex(K kern, dim3 grid, int threads, size_t smem, cudaStream_t 
   return e;
 }
 
-template <int NT, bool FUSED>
+template <int NT, bool FUSED, int AG>
 cudaError_t set_attr_once() {
   static bool done[64] = {false};  // per device: the attribute is per (function, device)
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
   if (done[dev]) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(head_stream_kernel<NT, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       ACfg<NT>::kSmemBytes);
+  cudaError_t e = cudaFuncSetAttribute(head_stream_kernel<NT, FUSED, AG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       ACfg<NT, AG>::kSmemBytes);
   if (e == cudaSuccess) done[dev] = true;
   return e;
 }
 
-template <int NP, int TPW>
+template <int NP, int TPW, bool MR>
 cudaError_t launch_select_cfg(const SplitArgs& b, cudaStream_t stream) {
   using C = BCfg<NP, TPW>;
   static bool done[64] = {false};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
   if (!done[dev]) {
-    const cudaError_t e = cudaFuncSetAttribute(head_select_kernel<NP, TPW>,
+    const cudaError_t e = cudaFuncSetAttribute(head_select_kernel<NP, TPW, MR>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
     if (e != cudaSuccess) return e;
     done[dev] = true;
   }
   const int pairs = b.p.batch * b.p.n;
-  return launch_ex(head_select_kernel<NP, TPW>, dim3((pairs + NP - 1) / NP), kBThreads, C::kSmem, stream, b);
+  return launch_ex(head_select_kernel<NP, TPW, MR>, dim3((pairs + NP - 1) / NP), kBThreads, C::kSmem, stream, b);
 }
 
 // Many (sequence, node) pairs whose tiles fit one round of the 4-pair layout
@@ -864,31 +938,40 @@ cudaError_t launch_select(const SplitArgs& b, int num_sms, cudaStream_t stream) 
   const int pairs = b.p.batch * b.p.n;
   const int ntp = b.tps + b.n_patch;
   if (pairs >= 4 * num_sms && ntp <= BCfg<4, 3>::kRound && b.S == 1 && b.extra == 0)
-    return launch_select_cfg<4, 3>(b, stream);
-  return launch_select_cfg<1, 1>(b, stream);
+    return launch_select_cfg<4, 3, false>(b, stream);
+  if (ntp > BCfg<1, 1>::kRound) return launch_select_cfg<1, 1, true>(b, stream);
+  return launch_select_cfg<1, 1, false>(b, stream);
 }
 
-template <int NT, bool FUSED>
+template <int NT, bool FUSED, int AG>
 cudaError_t launch_pair_of_kernels(const SplitArgs& a, int grid_a, cudaStream_t stream) {
-  cudaError_t e = set_attr_once<NT, FUSED>();
+  cudaError_t e = set_attr_once<NT, FUSED, AG>();
   if (e != cudaSuccess) return e;
   SplitArgs b = a;
   b.trace_base = grid_a;
   if (!(split_flags() & 16)) {  // experiment 16: kernel B alone (on the previous call's partials)
-    e = launch_ex(head_stream_kernel<NT, FUSED>, dim3(grid_a), kAThreads, ACfg<NT>::kSmemBytes, stream, a);
+    e = launch_ex(head_stream_kernel<NT, FUSED, AG>, dim3(grid_a), kAThreads, ACfg<NT, AG>::kSmemBytes, stream, a);
     if (e != cudaSuccess || (split_flags() & 1) || g_stream_only) return e;
   }
   return launch_select(b, num_sms_cached(), stream);
 }
 
+template <bool FUSED, int AG>
+cudaError_t launch_nt_ag(const SplitArgs& a, int grid_a, cudaStream_t stream) {
+  const int n = a.p.n;
+  if (n <= 16) return launch_pair_of_kernels<16, FUSED, AG>(a, grid_a, stream);
+  if (n <= 32) return launch_pair_of_kernels<32, FUSED, AG>(a, grid_a, stream);
+  if (n <= 64) return launch_pair_of_kernels<64, FUSED, AG>(a, grid_a, stream);
+  if (n <= 128) return launch_pair_of_kernels<128, FUSED, AG>(a, grid_a, stream);
+  return launch_pair_of_kernels<256, FUSED, 1>(a, grid_a, stream);  // 48 KB per atom: one atom per stage
+}
+
+// atoms per stage: 2 (256 contiguous bytes of a row per stage) unless the
+// experiment flag 32 asks for 1
 template <bool FUSED>
 cudaError_t launch_nt(const SplitArgs& a, int grid_a, cudaStream_t stream) {
-  const int n = a.p.n;
-  if (n <= 16) return launch_pair_of_kernels<16, FUSED>(a, grid_a, stream);
-  if (n <= 32) return launch_pair_of_kernels<32, FUSED>(a, grid_a, stream);
-  if (n <= 64) return launch_pair_of_kernels<64, FUSED>(a, grid_a, stream);
-  if (n <= 128) return launch_pair_of_kernels<128, FUSED>(a, grid_a, stream);
-  return launch_pair_of_kernels<256, FUSED>(a, grid_a, stream);
+  if (split_flags() & 32) return launch_nt_ag<FUSED, 1>(a, grid_a, stream);
+  return launch_nt_ag<FUSED, 2>(a, grid_a, stream);
 }
 
 SplitArgs base_args(const HeadProblem& p, int k, float* topk_logit, int32_t* topk_id, float* lse, void* scratch,
@@ -907,7 +990,6 @@ SplitArgs base_args(const HeadProblem& p, int k, float* topk_logit, int32_t* top
   a.k = k;
   a.tps = (p.max_ids + kBM - 1) / kBM;
   a.dbg_ld = p.max_ids;
-  a.w_evict_first = (split_flags() & 8) ? 1 : 0;
   return a;
 }
 
