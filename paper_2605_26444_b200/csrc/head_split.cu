@@ -60,15 +60,15 @@ constexpr int kMaxS = 32;          // K splits per tile
 constexpr int kMaxK = 32;
 constexpr long long kSpin = 1ll << 30;  // updater's arrival poll bound (a trap beats a hung GPU)
 
-template <int NT, int AG = 1>  // AG: 64-column K atoms per pipeline stage
+template <int NT, int AG = 1, int UT = 1>  // AG: 64-column K atoms per stage; UT: 128-row tiles per unit
 struct ACfg {
-  static constexpr int kAtomA = kBM * kBK * 2;    // 16 KB of W rows per atom
+  static constexpr int kAtomA = UT * kBM * kBK * 2;  // UT x 16 KB of W rows per atom
   static constexpr int kAtomB = NT * kBK * 2;     // NT x 128 B of H per atom
   static constexpr int kABytes = AG * kAtomA;
   static constexpr int kBBytes = AG * kAtomB;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStages = (kBudget / kStageBytes) > 8 ? 8 : (kBudget / kStageBytes);
-  static constexpr int kTmemCols = NT < 32 ? 32 : NT;
+  static constexpr int kTmemCols = UT * NT < 32 ? 32 : UT * NT;
   static constexpr int kStageArea = kStages * kStageBytes;
   static constexpr int kSmemBytes = kStageArea + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int kColGroups = NT / 16 < 4 ? NT / 16 : 4;  // drain column groups
@@ -82,6 +82,8 @@ struct SplitArgs {
   int n_patch;          // fused step: patch tiles (raw update-list entries, 128 per tile)
   int ntiles;           // batch * tps + n_patch; global tile t: regular (t / tps, t % tps), then patch tiles
   int S, extra;         // K splits: tiles t < extra take S + 1, the others S (every SM busy)
+  int ut;               // 128-row tiles per unit: 2 in the persistent split-K-1 mode (two MMAs share H)
+  int upt;              // units per sequence when ut == 2: ceil(tps / 2)
   int units;            // sum of the tiles' splits
   int heads;            // streaming CTAs (the fused grid has one more: the updater)
   // fused step (batch 1)
@@ -161,6 +163,17 @@ struct UnitPlan {
   int seq, tile, split, S, base, kb0, nk;
 };
 __device__ __forceinline__ UnitPlan plan_unit(const SplitArgs& a, int u) {
+  if (a.ut == 2) {  // two consecutive tiles of one sequence, full K (split-K 1)
+    UnitPlan r;
+    r.seq = u / a.upt;
+    r.tile = 2 * (u - r.seq * a.upt);
+    r.split = 0;
+    r.S = 1;
+    r.base = r.seq * a.tps + r.tile;
+    r.kb0 = 0;
+    r.nk = a.p.d / kBK;
+    return r;
+  }
   const Unit un = unit_of(a, u);
   UnitPlan r;
   r.seq = un.seq; r.tile = un.tile; r.split = un.split; r.S = un.S; r.base = un.base;
@@ -220,15 +233,16 @@ struct SplitPublish {
 };
 
 // ------------------------------------------------------------------ kernel A
-template <int NT, bool FUSED, int AG>
+template <int NT, bool FUSED, int AG, int UT>
 __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_constant__ SplitArgs a) {
-  using C = ACfg<NT, AG>;
+  using C = ACfg<NT, AG, UT>;
+  constexpr int kRows = kBM * UT;  // rows per unit
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStageArea);
   // bars[0..St) full, [St..2St) empty, [2St] tmem_full, [2St+1] tmem_empty
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::kStages + 2);
-  __shared__ int32_t ids_s[2][kBM];  // the unit's row ids (double-buffered: the next unit's are prefetched)
+  __shared__ int32_t ids_s[2][kBM * UT];  // the unit's row ids (double-buffered: the next unit's are prefetched)
   __shared__ int sh_m[2];
 
   const HeadProblem& p = a.p;
@@ -290,10 +304,10 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
     auto fetch_ids = [&](const UnitPlan& un, int buf) {
       if (un.tile < a.tps) {
         const int row0 = un.tile * kBM;
-        if (tid < kBM)
+        if (tid < kRows)
           ids_s[buf][tid] = row0 + tid < p.max_ids ? __ldcg(p.ids_base + (long long)un.seq * p.ids_stride + row0 + tid)
                                                    : -1;
-        if (tid == kBM) sh_m[buf] = clamp_nact(p, un.seq) - row0;
+        if (tid == kRows) sh_m[buf] = clamp_nact(p, un.seq) - row0;
       } else {  // patch rows: the raw update-list entries (invalid / foreign ids are not streamed)
         const int e = (un.tile - a.tps) * kBM + tid;
         if (tid < kBM) {
@@ -311,14 +325,14 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
     for (int u = blockIdx.x; u < a.units; u += stride, ++local) {
       const int buf = local & 1;
       const UnitPlan un = cur;
-      const int rows = min(kBM, sh_m[buf]);  // rows of this tile in the row list (<= 0: none)
+      const int rows = min(kRows, sh_m[buf]);  // rows of this unit in the row list (<= 0: none)
       if (FUSED && !arrived && tid == kLoaders) {  // pre-update slots read (the MMA warp: no loader stalls)
         red_add_release(a.arrive_ctr, 1u);
         arrived = true;
       }
       // the tile's row ids for B (split 0 only); rows past the list: -1
-      if (un.split == 0 && un.tile == 0 && tid == kBM) a.mrows[un.seq] = sh_m[buf];
-      if (un.split == 0 && tid < kBM) {
+      if (un.split == 0 && un.tile == 0 && tid == kRows) a.mrows[un.seq] = sh_m[buf];
+      if (un.split == 0 && tid < kRows && (un.tile >= a.tps || un.tile * kBM + tid < a.tps * kBM)) {
         const int32_t g = tid < rows ? ids_s[buf][tid] : -1;
         a.rowgid[((long long)un.seq * (a.tps + a.n_patch) + un.tile) * kBM + tid] = g;
       }
@@ -331,14 +345,14 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
         cur = n2;
         if (n2.tile < a.tps) {
           const int row0 = n2.tile * kBM;
-          if (tid < kBM && row0 + tid < p.max_ids) nx_id = __ldcg(p.ids_base + (long long)n2.seq * p.ids_stride + row0 + tid);
-          if (tid == kBM) nx_m = clamp_nact(p, n2.seq) - row0;
+          if (tid < kRows && row0 + tid < p.max_ids) nx_id = __ldcg(p.ids_base + (long long)n2.seq * p.ids_stride + row0 + tid);
+          if (tid == kRows) nx_m = clamp_nact(p, n2.seq) - row0;
         }
       }
       if (rows <= 0) {
         if (nx) {
-          if (tid < kBM) ids_s[buf ^ 1][tid] = nx_id;
-          if (tid == kBM) sh_m[buf ^ 1] = nx_m;
+          if (tid < kRows) ids_s[buf ^ 1][tid] = nx_id;
+          if (tid == kRows) sh_m[buf ^ 1] = nx_m;
         }
         __syncthreads();
         continue;
@@ -347,9 +361,9 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
       const int nst = (nk + AG - 1) / AG;  // pipeline stages of this unit
       if (warp < kLW) {
         // ---------------- loaders: rows of W_head + H into SW128 stages
-        const uint16_t* rp[2];
+        const uint16_t* rp[2 * UT];
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < 2 * UT; ++i) {
           const int r = lr + 64 * i;
           const int32_t g = r < rows ? ids_s[buf][r] : -1;
           const long long row = p.n_shards > 1 ? g / p.n_shards : g;
@@ -369,7 +383,7 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
             const uint32_t sB = sA + C::kABytes;
             // a row's AG atoms back to back: AG * 128 contiguous bytes per row per stage
 #pragma unroll
-            for (int i = 0; i < 2; ++i)
+            for (int i = 0; i < 2 * UT; ++i)
 #pragma unroll
               for (int at = 0; at < AG; ++at) {
                 const bool in = q * AG + at < nk;
@@ -409,15 +423,19 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
         const int lg = warp & 3, cgp = warp >> 2;
         const int r = lg * 32 + lane;  // TMEM lane == tile row
         const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16);
-        float* Pw = a.part + ((long long)(un.base + un.split) * p.n) * kBM + r;
-        if (cgp < C::kColGroups) {
-#pragma unroll 1
-          for (int c0 = cgp * 16; c0 < NT && c0 < p.n; c0 += 16 * C::kColGroups) {
-            float v[16];
-            tmem_ld16(taddr + c0, v);
 #pragma unroll
-            for (int c = 0; c < 16; ++c)
-              if (c0 + c < p.n) Pw[(c0 + c) * kBM] = v[c];
+        for (int h = 0; h < UT; ++h) {  // tile h of the unit: TMEM columns [h NT, (h + 1) NT)
+          if (UT > 1 && un.tile + h >= a.tps) break;
+          float* Pw = a.part + ((long long)(un.base + un.split + h) * p.n) * kBM + r;
+          if (cgp < C::kColGroups) {
+#pragma unroll 1
+            for (int c0 = cgp * 16; c0 < NT && c0 < p.n; c0 += 16 * C::kColGroups) {
+              float v[16];
+              tmem_ld16(taddr + h * NT + c0, v);
+#pragma unroll
+              for (int c = 0; c < 16; ++c)
+                if (c0 + c < p.n) Pw[(c0 + c) * kBM] = v[c];
+            }
           }
         }
         tc_fence_before();
@@ -442,8 +460,10 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
               if (q * AG + at < nk) {
 #pragma unroll
                 for (int kk = 0; kk < kBK / 16; ++kk)
-                  umma_bf16(tmem, sw128_desc(sA + at * C::kAtomA + kk * 32), sw128_desc(sB + at * C::kAtomB + kk * 32),
-                            idesc, (q | at | kk) ? 1u : 0u);
+#pragma unroll
+                  for (int h = 0; h < UT; ++h)  // the UT tiles share the H operand
+                    umma_bf16(tmem + h * NT, sw128_desc(sA + at * C::kAtomA + h * (kBM * 128) + kk * 32),
+                              sw128_desc(sB + at * C::kAtomB + kk * 32), idesc, (q | at | kk) ? 1u : 0u);
               }
             umma_commit(smem_u32(&bars[C::kStages + stage]));
             if (q == nst - 1) umma_commit(smem_u32(&bars[2 * C::kStages]));
@@ -454,8 +474,8 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
       it += nst;
       ++nrun;
       if (nx) {
-        if (tid < kBM) ids_s[buf ^ 1][tid] = nx_id;
-        if (tid == kBM) sh_m[buf ^ 1] = nx_m;
+        if (tid < kRows) ids_s[buf ^ 1][tid] = nx_id;
+        if (tid == kRows) sh_m[buf ^ 1] = nx_m;
       }
       __syncthreads();  // ids_s[buf] free; the next unit's ids in ids_s[buf ^ 1]
     }
@@ -860,7 +880,7 @@ int g_num_sms = 148;  // set by the launchers (the select kernel's layout choice
 int num_sms_cached() { return g_num_sms; }
 int g_stream_only = 0;  // debug mode 1: kernel A alone (measurement; no outputs are written)
 // experiments (NANOSPEC_SPLIT_FLAGS): 1 = skip kernel B, 2 = no PDL, 16 = kernel B alone,
-// 32 = one K atom per pipeline stage
+// 32 = one K atom per pipeline stage, 64 = no 256-row units in the persistent mode
 int g_split_flags = -1;
 int split_flags() {
   if (g_split_flags < 0) {
@@ -904,14 +924,14 @@ cudaError_t launch_ex(K kern, dim3 grid, int threads, size_t smem, cudaStream_t 
   return e;
 }
 
-template <int NT, bool FUSED, int AG>
+template <int NT, bool FUSED, int AG, int UT>
 cudaError_t set_attr_once() {
   static bool done[64] = {false};  // per device: the attribute is per (function, device)
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
   if (done[dev]) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(head_stream_kernel<NT, FUSED, AG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       ACfg<NT, AG>::kSmemBytes);
+  cudaError_t e = cudaFuncSetAttribute(head_stream_kernel<NT, FUSED, AG, UT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, ACfg<NT, AG, UT>::kSmemBytes);
   if (e == cudaSuccess) done[dev] = true;
   return e;
 }
@@ -943,14 +963,15 @@ cudaError_t launch_select(const SplitArgs& b, int num_sms, cudaStream_t stream) 
   return launch_select_cfg<1, 1, false>(b, stream);
 }
 
-template <int NT, bool FUSED, int AG>
+template <int NT, bool FUSED, int AG, int UT>
 cudaError_t launch_pair_of_kernels(const SplitArgs& a, int grid_a, cudaStream_t stream) {
-  cudaError_t e = set_attr_once<NT, FUSED, AG>();
+  cudaError_t e = set_attr_once<NT, FUSED, AG, UT>();
   if (e != cudaSuccess) return e;
   SplitArgs b = a;
   b.trace_base = grid_a;
   if (!(split_flags() & 16)) {  // experiment 16: kernel B alone (on the previous call's partials)
-    e = launch_ex(head_stream_kernel<NT, FUSED, AG>, dim3(grid_a), kAThreads, ACfg<NT, AG>::kSmemBytes, stream, a);
+    e = launch_ex(head_stream_kernel<NT, FUSED, AG, UT>, dim3(grid_a), kAThreads, ACfg<NT, AG, UT>::kSmemBytes,
+                  stream, a);
     if (e != cudaSuccess || (split_flags() & 1) || g_stream_only) return e;
   }
   return launch_select(b, num_sms_cached(), stream);
@@ -959,17 +980,28 @@ cudaError_t launch_pair_of_kernels(const SplitArgs& a, int grid_a, cudaStream_t 
 template <bool FUSED, int AG>
 cudaError_t launch_nt_ag(const SplitArgs& a, int grid_a, cudaStream_t stream) {
   const int n = a.p.n;
-  if (n <= 16) return launch_pair_of_kernels<16, FUSED, AG>(a, grid_a, stream);
-  if (n <= 32) return launch_pair_of_kernels<32, FUSED, AG>(a, grid_a, stream);
-  if (n <= 64) return launch_pair_of_kernels<64, FUSED, AG>(a, grid_a, stream);
-  if (n <= 128) return launch_pair_of_kernels<128, FUSED, AG>(a, grid_a, stream);
-  return launch_pair_of_kernels<256, FUSED, 1>(a, grid_a, stream);  // 48 KB per atom: one atom per stage
+  if (n <= 16) return launch_pair_of_kernels<16, FUSED, AG, 1>(a, grid_a, stream);
+  if (n <= 32) return launch_pair_of_kernels<32, FUSED, AG, 1>(a, grid_a, stream);
+  if (n <= 64) return launch_pair_of_kernels<64, FUSED, AG, 1>(a, grid_a, stream);
+  if (n <= 128) return launch_pair_of_kernels<128, FUSED, AG, 1>(a, grid_a, stream);
+  return launch_pair_of_kernels<256, FUSED, 1, 1>(a, grid_a, stream);  // 48 KB per atom: one atom per stage
+}
+
+// Persistent split-K-1 mode with 256-row units (two tiles share every H stage):
+// one atom per stage (40 KB at n <= 64: four stages).
+cudaError_t launch_nt_ut2(const SplitArgs& a, int grid_a, cudaStream_t stream) {
+  const int n = a.p.n;
+  if (n <= 16) return launch_pair_of_kernels<16, false, 1, 2>(a, grid_a, stream);
+  if (n <= 32) return launch_pair_of_kernels<32, false, 1, 2>(a, grid_a, stream);
+  if (n <= 64) return launch_pair_of_kernels<64, false, 1, 2>(a, grid_a, stream);
+  return launch_pair_of_kernels<128, false, 1, 2>(a, grid_a, stream);
 }
 
 // atoms per stage: 2 (256 contiguous bytes of a row per stage) unless the
 // experiment flag 32 asks for 1
 template <bool FUSED>
 cudaError_t launch_nt(const SplitArgs& a, int grid_a, cudaStream_t stream) {
+  if (!FUSED && a.ut == 2) return launch_nt_ut2(a, grid_a, stream);
   if (split_flags() & 32) return launch_nt_ag<FUSED, 1>(a, grid_a, stream);
   return launch_nt_ag<FUSED, 2>(a, grid_a, stream);
 }
@@ -1031,6 +1063,15 @@ cudaError_t launch_head_tc(const HeadProblem& p, int k, float* topk_logit, int32
   a.n_patch = 0;
   a.ntiles = p.batch * a.tps;
   plan_splits(a, G, p.d / kBK);
+  a.ut = 1;
+  if (a.S == 1 && a.ntiles > G && (p.batch > 1 || a.ntiles >= 2 * G) && p.n <= 128 && !(split_flags() & 64)) {
+    // more tiles than SMs: 256-row units, two MMAs per K step sharing the hidden-state stage.
+    // Not for one sequence of capacity < 2 x SMs tiles: its live tiles may be far
+    // fewer (the host cannot see n_active), and halving the units would idle SMs.
+    a.ut = 2;
+    a.upt = (a.tps + 1) / 2;
+    a.units = p.batch * a.upt;
+  }
   a.heads = a.units < G ? a.units : G;
   return launch_nt<false>(a, a.heads, stream);
 }

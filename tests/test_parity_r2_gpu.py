@@ -236,3 +236,24 @@ def test_repack_variant_matches(cuda_ok, llama):
         assert torch.equal(i1, i2) and torch.equal(v1, v2) and torch.equal(l1, l2), f"step {s}"
         slots = st.read(0)["slots"]
         assert torch.equal(ph.packed[0, : len(slots)], W[torch.as_tensor(slots, device="cuda").long()])
+
+
+def test_persistent_odd_tile_count(cuda_ok, llama):
+    """The persistent split-K-1 mode with 256-row units when a sequence has an
+    odd number of row tiles (W_max 2900 -> 23 tiles, 8 sequences: 184 tiles >
+    148 SMs): the last unit of every sequence holds one tile."""
+    from paper_2605_26444_b200 import ActiveVocab, draft_logits_topk
+    W, Wb = llama
+    V, d = W.shape
+    B, n, k, Wm = 8, 60, 10, 2900
+    st = ActiveVocab(V, Wm, batch=B)
+    rng = np.random.default_rng(17)
+    for b in range(B):
+        st.init(b, _t(rng.choice(V, Wm - 37 * b, replace=False)))
+    H = SI.bf16_hidden(n, d, seed=29, device="cuda", batch=B)
+    v, i, l, zz = draft_logits_topk(st, W, H, k, debug_logits=True)
+    torch.cuda.synchronize()
+    for b in (0, 3, 7):
+        ids = st.read(b)["slots"]
+        _check(v[b].cpu().numpy(), i[b].cpu().numpy(), l[b].cpu().numpy(), ids, Wb, H[b], k, f"odd tiles seq {b}",
+               zz[b, :, : len(ids)].cpu().numpy())
