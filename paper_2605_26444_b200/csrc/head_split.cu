@@ -880,7 +880,8 @@ int g_num_sms = 148;  // set by the launchers (the select kernel's layout choice
 int num_sms_cached() { return g_num_sms; }
 int g_stream_only = 0;  // debug mode 1: kernel A alone (measurement; no outputs are written)
 // experiments (NANOSPEC_SPLIT_FLAGS): 1 = skip kernel B, 2 = no PDL, 16 = kernel B alone,
-// 32 = one K atom per pipeline stage, 64 = no 256-row units in the persistent mode
+// 32 = one K atom per pipeline stage, 64 = no 256-row units in the persistent mode,
+// 128 = two K atoms per stage with 256-row units
 int g_split_flags = -1;
 int split_flags() {
   if (g_split_flags < 0) {
@@ -989,12 +990,17 @@ cudaError_t launch_nt_ag(const SplitArgs& a, int grid_a, cudaStream_t stream) {
 
 // Persistent split-K-1 mode with 256-row units (two tiles share every H stage):
 // one atom per stage (40 KB at n <= 64: four stages).
-cudaError_t launch_nt_ut2(const SplitArgs& a, int grid_a, cudaStream_t stream) {
+template <int AG>
+cudaError_t launch_nt_ut2_ag(const SplitArgs& a, int grid_a, cudaStream_t stream) {
   const int n = a.p.n;
-  if (n <= 16) return launch_pair_of_kernels<16, false, 1, 2>(a, grid_a, stream);
-  if (n <= 32) return launch_pair_of_kernels<32, false, 1, 2>(a, grid_a, stream);
-  if (n <= 64) return launch_pair_of_kernels<64, false, 1, 2>(a, grid_a, stream);
+  if (n <= 16) return launch_pair_of_kernels<16, false, AG, 2>(a, grid_a, stream);
+  if (n <= 32) return launch_pair_of_kernels<32, false, AG, 2>(a, grid_a, stream);
+  if (n <= 64) return launch_pair_of_kernels<64, false, AG, 2>(a, grid_a, stream);
   return launch_pair_of_kernels<128, false, 1, 2>(a, grid_a, stream);
+}
+cudaError_t launch_nt_ut2(const SplitArgs& a, int grid_a, cudaStream_t stream) {
+  if (split_flags() & 128) return launch_nt_ut2_ag<2>(a, grid_a, stream);  // experiment: 2 atoms per stage
+  return launch_nt_ut2_ag<1>(a, grid_a, stream);
 }
 
 // atoms per stage: 2 (256 contiguous bytes of a row per stage) unless the

@@ -127,3 +127,33 @@ if args.trace:
             if len(c):
                 r_ = (c - t0) / 1e3
                 print(f"    {name:16s} n={len(c):3d} min {r_.min():6.2f} med {np.median(r_):6.2f} max {r_.max():6.2f}")
+
+if args.trace:
+    # three consecutive steps (head-only, then fused) captured in ONE graph, each
+    # with its own trace region: the overlap / gaps between consecutive launches
+    for what in ("head", "step"):
+        regs = [torch.zeros(1024 * 16, dtype=torch.int64, device=dev) for _ in range(3)]
+        fn = head_cold if what == "head" else step_cold
+        for s in range(3):
+            fn(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for s in range(3):
+                N.check(N.lib().nanospec_debug_set_trace(regs[s].data_ptr(), 1024), "trace")
+                fn(10 + s)
+        N.check(N.lib().nanospec_debug_set_trace(None, 0), "trace")
+        g.replay()
+        torch.cuda.synchronize()
+        ts = [r.view(1024, 16).cpu().numpy().astype(np.int64) for r in regs]
+        t0 = min(t[t[:, 0] > 0, 0].min() for t in ts)
+        print(f"graph of 3 {what} calls (us from the first stream CTA start):")
+        for s, t in enumerate(ts):
+            nA = int(np.argmax(t[:, 12] == 0xB)) if (t[:, 12] == 0xB).any() else int((t[:, 0] > 0).sum())
+            A, B = t[:nA], t[nA:nA + 512]
+            B = B[B[:, 12] == 0xB]
+            def rng(c):
+                c = c[c > 0]
+                return f"{(c.min() - t0) / 1e3:6.2f}..{(c.max() - t0) / 1e3:6.2f}" if len(c) else "-"
+            print(f"  call {s}: A start {rng(A[:, 0])} dep {rng(A[:, 1])} first loads {rng(A[:, 2])} "
+                  f"drained {rng(A[:, 9])} | B start {rng(B[:, 0])} dep {rng(B[:, 1])} done {rng(B[:, 4])}")
