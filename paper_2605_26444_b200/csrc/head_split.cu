@@ -192,29 +192,31 @@ __device__ __forceinline__ int32_t list_entry(const AppendArgs& u, int e) {
 struct SplitPublish {
   const SplitArgs* a;
   uint32_t* words;  // shared: (tps + n_patch) * 4 drop words
-  int32_t* list;    // shared: the raw update lists (L entries)
   __device__ void operator()(const StateView& sv, UpdSmem& sm, int n_old, int nl, int ne) const {
     const int tid = threadIdx.x, nt = blockDim.x;
     const int nw = (a->tps + a->n_patch) * 4;
     const int L = a->L;
+    const int32_t* list = sm.raw;  // the raw update lists, staged by update_fast in its first round trip
+    // the streaming CTAs' arrivals (long complete by now): the acquire load is
+    // issued here and checked after the drop bitmap, so its round trip overlaps
+    unsigned arrived = 0u;
+    if (tid == 0) arrived = ld_acquire(a->arrive_ctr);
     for (int w = tid; w < nw; w += nt) words[w] = 0u;
-    for (int t = tid; t < L; t += nt) list[t] = list_entry(a->upd, t);
     __syncthreads();
     // pre-update slots whose id left I (the slot of every leaving id, hole[q])
     for (int q = tid; q < nl; q += nt) atomicOr(&words[sm.hole[q] >> 5], 1u << (sm.hole[q] & 31));
     // a patch row counts iff it is the first entry of its id, valid, on this
     // shard, and its id enters I
-    for (int t = tid; t < L; t += nt) {
+    for (int t = tid; t < L; t += nt) {  // no early exits: the shared-memory loads pipeline
       const int32_t g = list[t];
-      bool counts = g >= 0 && g < sv.vocab && is_local(sv, g);
-      for (int q = 0; counts && q < t; ++q) counts = list[q] != g;
-      if (counts) {
-        const int32_t lg = local_of(sv, g);
-        bool in = false;
-        for (int q = 0; q < ne && !in; ++q) in = sm.enter[q] == lg;
-        counts = in;
-      }
-      if (!counts) atomicOr(&words[a->tps * 4 + (t >> 5)], 1u << (t & 31));
+      const bool valid = g >= 0 && g < sv.vocab && is_local(sv, g);
+      const int32_t lg = valid ? local_of(sv, g) : -1;
+      bool dup = false, in = false;
+#pragma unroll 8
+      for (int q = 0; q < t; ++q) dup |= list[q] == g;
+#pragma unroll 8
+      for (int q = 0; q < ne; ++q) in |= sm.enter[q] == lg;
+      if (!(valid && !dup && in)) atomicOr(&words[a->tps * 4 + (t >> 5)], 1u << (t & 31));
     }
     __syncthreads();
     for (int w = tid; w < nw; w += nt) a->drop[w] = words[w];
@@ -223,10 +225,11 @@ struct SplitPublish {
       // then may ids[], pos[] and meta change (one-way wait: the streaming
       // CTAs never wait, so they always get to arrive)
       long long spins = 0;
-      while (ld_acquire(a->arrive_ctr) != (unsigned)a->heads)
+      while (arrived != (unsigned)a->heads) {
+        arrived = ld_acquire(a->arrive_ctr);
         if (++spins > kSpin) __trap();
-      *a->arrive_ctr = 0u;
-      __threadfence();
+      }
+      *a->arrive_ctr = 0u;  // visible to the next launch at this grid's completion
     }
     __syncthreads();
   }
@@ -289,9 +292,8 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
     uint8_t* base = smem;
     UpdSmem& us = *reinterpret_cast<UpdSmem*>(base);
     uint32_t* words = reinterpret_cast<uint32_t*>(base + (sizeof(UpdSmem) + 255) / 256 * 256);
-    int32_t* list = reinterpret_cast<int32_t*>(words + (a.tps + a.n_patch) * 4);
-    SplitPublish pub{&a, words, list};
-    update_fast(a.upd, a.upd.seq0, us, pub, nullptr);
+    SplitPublish pub{&a, words};
+    update_fast(a.upd, a.upd.seq0, us, pub, p.trace);
     if (tid == 0) trace_mark(p.trace, 11);
   } else {
     constexpr uint32_t idesc = make_idesc(kBM, NT);
@@ -881,7 +883,7 @@ int num_sms_cached() { return g_num_sms; }
 int g_stream_only = 0;  // debug mode 1: kernel A alone (measurement; no outputs are written)
 // experiments (NANOSPEC_SPLIT_FLAGS): 1 = skip kernel B, 2 = no PDL, 16 = kernel B alone,
 // 32 = one K atom per pipeline stage, 64 = no 256-row units in the persistent mode,
-// 128 = two K atoms per stage with 256-row units
+// 128 = one K atom per stage with 256-row units
 int g_split_flags = -1;
 int split_flags() {
   if (g_split_flags < 0) {
@@ -999,8 +1001,8 @@ cudaError_t launch_nt_ut2_ag(const SplitArgs& a, int grid_a, cudaStream_t stream
   return launch_pair_of_kernels<128, false, 1, 2>(a, grid_a, stream);
 }
 cudaError_t launch_nt_ut2(const SplitArgs& a, int grid_a, cudaStream_t stream) {
-  if (split_flags() & 128) return launch_nt_ut2_ag<2>(a, grid_a, stream);  // experiment: 2 atoms per stage
-  return launch_nt_ut2_ag<1>(a, grid_a, stream);
+  if (split_flags() & 128) return launch_nt_ut2_ag<1>(a, grid_a, stream);  // experiment: 1 atom per stage
+  return launch_nt_ut2_ag<2>(a, grid_a, stream);  // 2 atoms x 2 tiles per stage, two stages in flight
 }
 
 // atoms per stage: 2 (256 contiguous bytes of a row per stage) unless the

@@ -63,6 +63,7 @@ struct UpdSmem {
   int32_t hval[kHashSlots];   // first position, then net count change
   int32_t hcnt[kHashSlots];   // window count before this update
   int32_t hpos[kHashSlots];   // slot before this update (evicted ids)
+  int32_t raw[kFastThreads];    // the update lists as given (draft, then verify), for the publish hook
   int32_t leave[kFastThreads];  // local ids leaving I
   int32_t enter[kFastThreads];  // local ids entering I
   int32_t hole[kFastThreads];   // their former slots
@@ -115,6 +116,7 @@ __device__ void update_fast(const AppendArgs& args, int seq, UpdSmem& sm, Publis
   if (tid < la) e = args.a.ptr[(long long)(seq - args.seq0) * args.a.seq_stride + tid];
   else if (tid < L) e = args.b.ptr[(long long)(seq - args.seq0) * args.b.seq_stride + (tid - la)];
   for (int h = tid; h < kHashSlots; h += blockDim.x) { hkey[h] = -1; hval[h] = 0x7fffffff; }
+  if (tid < L) sm.raw[tid] = e;
   __syncthreads();
   if (tid == 0) trace_mark(trace, 10);  // state: lists staged
   // ---- tuple(.): keep the first occurrence of every id within its own list

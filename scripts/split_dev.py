@@ -106,6 +106,11 @@ if args.trace:
         # A rows are a contiguous block from 0; B rows follow
         nA = int(np.argmax(t[:, 12] == 0xB)) if (t[:, 12] == 0xB).any() else int(live.sum())
         print(f"trace {'head' if it == 0 else 'fused step'}: A CTAs {nA}, B CTAs {len(rows) - nA}")
+        if nA > 147 and t[nA - 1, 10] > 0:  # the fused step's updater (last stream CTA): its phases
+            u = t[nA - 1]
+            print("    updater: " + ", ".join(f"{nm} {(u[e] - t0) / 1e3:.2f}" for nm, e in
+                                           (("start", 0), ("dep", 1), ("lists", 10), ("ring", 11), ("counts", 12),
+                                            ("written", 14), ("exit", 9)) if u[e] > 0))
         for name, e in (("A start", 0), ("A dep", 1), ("A ids", 7), ("A first loads", 2), ("A loads landed", 3), ("A last MMA", 4),
                         ("A drained", 9), ("upd published", 11)):
             c = t[:nA, e]
