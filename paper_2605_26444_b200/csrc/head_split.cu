@@ -17,15 +17,26 @@
 // 128-byte store per node per warp).  It then exits: nothing in A waits for
 // another CTA.
 //
-// Kernel B (head_select_kernel, one CTA per (sequence, node)): waits for A
-// (griddepcontrol.wait: A complete, its stores visible), sums every row's S
-// partials in K-chunk order (one order for every tile: equal rows give
-// bit-equal logits), keeps the row only if it is in I, folds the lse online,
-// and selects the top-k: each warp keeps a running sorted top-k list (a batch
-// of 128 rows enters through a threshold -- the k-th largest lane maximum --
-// so only a few candidates are ranked), then one warp merges the warp lists
-// (threshold = k-th largest list head, rank by counting).  Global ids come
-// from the row-id table A wrote, so B never reads the state.
+// Kernel B (one CTA per (sequence, node)) waits for A (griddepcontrol.wait:
+// A complete, its stores visible) and sums every row's S partials in K-chunk
+// order (one order for every tile: equal rows give bit-equal logits); a row
+// counts only if it is in I.  head_select_tiles_kernel (<= 32 tiles: every
+// head of one sequence up to |I| = 4096): warp w reduces tile w to its top-k
+// list + (max, sum exp) (warp_topk4: threshold = k-th largest lane maximum by
+// a bitonic sort over lanes, the few keys above it ranked by counting), then
+// warp 0 merges the lists the same way and warp 1 folds the lse.
+// head_select_kernel (more tiles): rounds of 32 tiles with a two-pass radix
+// threshold.  Global ids come from the row-id table A wrote, so B never reads
+// the state.
+//
+// List mode (split-K 1, more tiles than SMs: dp64, the dense [0, V) head, a
+// 32k window): A gets 8 more warps.  The TMEM accumulator is double-buffered;
+// while the loaders stream unit j + 1, the epilogue warps stage unit j's
+// columns into shared memory and reduce every (tile, node) to its top-k list
+// + (max, sum exp) (warp_topk4); the CTA's last unit is reduced by all its
+// warps together once the stream is done.  head_merge_kernel then merges the
+// per-tile lists of each (sequence, node): a few hundred candidates instead of
+// |I| logits.
 //
 // Fused step (nanospec_step, one sequence): A streams a SUPERSET of the
 // post-update active set that is known without waiting for the update -- the
@@ -60,18 +71,30 @@ constexpr int kMaxS = 32;          // K splits per tile
 constexpr int kMaxK = 32;
 constexpr long long kSpin = 1ll << 30;  // updater's arrival poll bound (a trap beats a hung GPU)
 
-template <int NT, int AG = 1, int UT = 1>  // AG: 64-column K atoms per stage; UT: 128-row tiles per unit
+// List mode (persistent split-K 1): kEW epilogue warps reduce every finished
+// tile, straight from TMEM, to per-node top-k lists + lse partials while the
+// loaders stream the next unit (the TMEM accumulator is double-buffered).
+constexpr int kEW = 8;  // two per TMEM lane group: each stages half of a chunk's columns
+constexpr int kAThreadsL = kAThreads + kEW * 32;
+constexpr int kZCols = 64;                               // nodes per epilogue chunk
+constexpr int kListExtra = kZCols * kBM * 4 /*Z*/ + 2 * kBM * 4 /*row ids*/ + kEW * kBM * 8 /*candidates*/;
+constexpr int kListCap = 26000;                          // merge kernel: candidates per (sequence, node)
+
+template <int NT, int AG = 1, int UT = 1, bool LIST = false>  // AG: 64-column K atoms per stage; UT: 128-row tiles per unit
 struct ACfg {
   static constexpr int kAtomA = UT * kBM * kBK * 2;  // UT x 16 KB of W rows per atom
   static constexpr int kAtomB = NT * kBK * 2;     // NT x 128 B of H per atom
   static constexpr int kABytes = AG * kAtomA;
   static constexpr int kBBytes = AG * kAtomB;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (kBudget / kStageBytes) > 8 ? 8 : (kBudget / kStageBytes);
-  static constexpr int kTmemCols = UT * NT < 32 ? 32 : UT * NT;
+  static constexpr int kBud = LIST ? 224 * 1024 - kListExtra - 2048 : kBudget;
+  static constexpr int kStages = (kBud / kStageBytes) > 8 ? 8 : (kBud / kStageBytes);
+  static constexpr int kTmemCols = (LIST ? 2 : 1) * UT * NT < 32 ? 32 : (LIST ? 2 : 1) * UT * NT;
   static constexpr int kStageArea = kStages * kStageBytes;
-  static constexpr int kSmemBytes = kStageArea + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kExtra = LIST ? kListExtra : 0;     // after the barriers: Z, row ids, candidates
+  static constexpr int kSmemBytes = kStageArea + 1024 /*align*/ + 256 /*barriers*/ + kExtra;
   static constexpr int kColGroups = NT / 16 < 4 ? NT / 16 : 4;  // drain column groups
+  static_assert(kStages >= 2, "at least two pipeline stages");
 };
 
 struct SplitArgs {
@@ -97,6 +120,7 @@ struct SplitArgs {
   int32_t* topk_id;
   float* lse;           // [batch][n] or null
   int k;
+  long long list_stats; // list mode: byte offset (in part) of the [tiles][n] (M, sum exp) lse partials
   long long dbg_ld;     // debug logits: floats between the rows of one (sequence, node)
   int trace_base;       // debug trace: B's CTA b writes trace row trace_base + b (after A's rows)
 };
@@ -235,18 +259,241 @@ struct SplitPublish {
   }
 };
 
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// One warp, one (tile, node): the 128 logits zc[0, 128) of the tile's rows
+// (lane owns rows lane + 32 j, id gid[j], -1 = not in I) ->
+//   out[0, k)  the tile's top-k (key, id) by (value desc, id asc), padded with (0, -1)
+//   *stat      (M, sum exp(z - M)) over the rows in I (M = -inf: none)
+// Threshold T = the k-th largest lane maximum: k lanes own a key >= T, so every
+// top-k key is >= T; the few keys >= T are staged in cs (<= 128 entries) and
+// ranked by counting.
+__device__ __forceinline__ void warp_topk4(const uint32_t (&key)[4], const int32_t (&gid)[4], int k, uint2* cs,
+                                           uint2* out, float2* stat) {
+  const int lane = threadIdx.x & 31;
+  uint32_t lm = 0u;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) lm = key[j] > lm ? key[j] : lm;
+  // bitonic sort (ascending over lanes) of the lane maxima: lane 32 - k holds the k-th largest
+  uint32_t v = lm;
+#pragma unroll
+  for (int sz = 2; sz <= 32; sz <<= 1)
+#pragma unroll
+    for (int st = sz >> 1; st > 0; st >>= 1) {
+      const uint32_t o = __shfl_xor_sync(0xffffffffu, v, st);
+      const bool keep_min = ((lane & st) == 0) == ((lane & sz) == 0);
+      v = keep_min ? (o < v ? o : v) : (o > v ? o : v);
+    }
+  const uint32_t T = __shfl_sync(0xffffffffu, v, 32 - k);  // 0 when fewer than k lanes hold a row
+  const uint32_t mx = __shfl_sync(0xffffffffu, v, 31);
+  const float M = key_value(mx);
+  float es = 0.f;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (key[j]) es += __expf(key_value(key[j]) - M);
+  int cnt = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const bool in = key[j] != 0u && key[j] >= T;
+    const unsigned b = __ballot_sync(0xffffffffu, in);
+    if (in) cs[cnt + __popc(b & ((1u << lane) - 1u))] = make_uint2(key[j], (uint32_t)gid[j]);
+    cnt += __popc(b);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
+  __syncwarp();
+  for (int q = lane; q < cnt; q += 32) {
+    const uint2 me = cs[q];
+    int rk = 0;
+#pragma unroll 4
+    for (int f = 0; f < cnt; ++f) {
+      const uint2 o = cs[f];
+      rk += key_before(o.x, o.y, me.x, me.y) ? 1 : 0;
+    }
+    if (rk < k) out[rk] = me;
+  }
+  for (int q = cnt + lane; q < k; q += 32) out[q] = make_uint2(0u, 0xffffffffu);
+  if (lane == 0) *stat = make_float2(mx ? M : -INFINITY, es);
+  __syncwarp();  // cs reused by the caller's next call
+}
+
+__device__ __forceinline__ void warp_tile_topk(const float* zc, const int32_t (&gid)[4], int k, uint2* cs, uint2* out,
+                                               float2* stat, float* dbg) {
+  const int lane = threadIdx.x & 31;
+  uint32_t key[4];
+  float zv[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    zv[j] = zc[lane + 32 * j];
+    key[j] = gid[j] >= 0 ? float_key(zv[j]) : 0u;
+  }
+  warp_topk4(key, gid, k, cs, out, stat);
+  if (dbg) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (gid[j] >= 0) dbg[lane + 32 * j] = zv[j];
+  }
+}
+
+__device__ __forceinline__ int unit_rows(const SplitArgs& a, const UnitPlan& un, int ut) {
+  return min(kBM * ut, clamp_nact(a.p, un.seq) - un.tile * kBM);  // as the loaders compute it (non-fused)
+}
+
+// Per-CTA hand-off from the epilogue warps to the joint tail (list mode).
+struct ListTail {
+  int u, e;  // the CTA's last unit with rows and its index among those units (-1: none)
+};
+
+// ------------------------------------------------------------------ list-mode epilogue
+// The kEW epilogue warps of a persistent split-K-1 stream kernel: for every
+// unit this CTA streams (same order as the MMA warp) except its last one, wait
+// for its TMEM buffer, stage each 64-node chunk of each 128-row tile into
+// shared memory (node-major), release the buffer after its last read, and
+// reduce every (tile, node) with warp_tile_topk into
+//   list[tile][node][0, k), stats[tile][node].
+// The CTA's last unit is left to the joint tail (every warp of the CTA, once
+// the loaders and the MMA warp are done): its epilogue is the exposed part.
+template <int NT, int UT>
+__device__ __forceinline__ void list_epilogue(const SplitArgs& a, uint32_t tmem, uint64_t* tbars, float* Z,
+                                              int32_t* gid_s, uint2* cand, ListTail* tail) {
+  // tbars[2b] = tmem_full of buffer b, tbars[2b + 1] = its tmem_empty
+  const HeadProblem& p = a.p;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ew = warp - (kLW + 1), etid = tid - (kLW + 1) * 32;
+  const int lg = warp & 3;  // TMEM lane group this warp may read
+  const int k = a.k;
+  uint2* cs = cand + ew * kBM;
+  uint2* lists = reinterpret_cast<uint2*>(a.part);
+  float2* stats = reinterpret_cast<float2*>(reinterpret_cast<char*>(a.part) + a.list_stats);
+  int e = 0;
+  int u = blockIdx.x;
+  UnitPlan un = plan_unit(a, u < a.units ? u : 0);
+  int rows = u < a.units ? unit_rows(a, un, UT) : 0;
+  while (u < a.units && rows <= 0) {  // the first unit with rows
+    u += a.heads;
+    if (u < a.units) { un = plan_unit(a, u); rows = unit_rows(a, un, UT); }
+  }
+  while (u < a.units) {
+    // the next unit with rows (none: this one is the CTA's last -> the joint tail)
+    int u2 = u + a.heads, rows2 = 0;
+    UnitPlan un2 = un;
+    while (u2 < a.units) {
+      un2 = plan_unit(a, u2);
+      rows2 = unit_rows(a, un2, UT);
+      if (rows2 > 0) break;
+      u2 += a.heads;
+    }
+    if (u2 >= a.units) {
+      if (etid == 0) { tail->u = u; tail->e = e; }
+      return;
+    }
+    const int32_t* ids = p.ids_base + (long long)un.seq * p.ids_stride + un.tile * kBM;
+    for (int r = etid; r < kBM * UT; r += kEW * 32) gid_s[r] = r < rows ? __ldcg(ids + r) : -1;
+    const int tb = e & 1;
+    mbar_wait(smem_u32(&tbars[2 * tb]), (e >> 1) & 1);
+    tc_fence_after();
+    const int nh = (rows + kBM - 1) / kBM;
+    const int ncc = (p.n + kZCols - 1) / kZCols;
+    for (int h = 0; h < nh; ++h) {
+      const long long gt = (long long)un.seq * a.tps + un.tile + h;  // global tile
+      for (int cc = 0; cc < ncc; ++cc) {
+        const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + tb * UT * NT + h * NT + cc * kZCols;
+        const int r = lg * 32 + lane;
+#pragma unroll
+        for (int c16 = 0; c16 < kZCols / 16; ++c16) {
+          if (c16 % (kEW / 4) == ew / 4 && cc * kZCols + c16 * 16 < NT && cc * kZCols + c16 * 16 < p.n) {
+            float v[16];
+            tmem_ld16(taddr + c16 * 16, v);
+#pragma unroll
+            for (int c = 0; c < 16; ++c) Z[(c16 * 16 + c) * kBM + r] = v[c];
+          }
+        }
+        if (h == nh - 1 && cc == ncc - 1) {  // the last read of this TMEM buffer
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&tbars[2 * tb + 1]));
+        }
+        named_sync(2, kEW * 32);  // Z (and, the first time, gid_s) complete
+        int32_t gid[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) gid[j] = gid_s[h * kBM + lane + 32 * j];
+        const int cn = min(kZCols, p.n - cc * kZCols);
+        for (int c = ew; c < cn; c += kEW) {
+          const int node = cc * kZCols + c;
+          warp_tile_topk(Z + c * kBM, gid, k, cs, lists + (gt * p.n + node) * k, stats + gt * p.n + node,
+                         p.logits ? p.logits + ((long long)un.seq * p.n + node) * a.dbg_ld + (un.tile + h) * kBM
+                                  : nullptr);
+        }
+        named_sync(2, kEW * 32);  // Z free
+      }
+    }
+    ++e;
+    u = u2;
+    un = un2;
+    rows = rows2;
+  }
+  if (etid == 0) { tail->u = -1; tail->e = -1; }
+}
+
+// The joint tail (list mode): every warp of the CTA reduces the CTA's last
+// unit -- the 16 loader warps stage each tile's TMEM columns into the (now
+// idle) stage area, then all warps share its (tile, node) reductions.
+template <int NT, int UT>
+__device__ __forceinline__ void list_tail(const SplitArgs& a, uint32_t tmem, uint64_t* tbars, float* Zt,
+                                          int32_t* gid_s, uint2* cand, const ListTail& tail) {
+  const HeadProblem& p = a.p;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int kWarps = kAThreadsL / 32;
+  const int k = a.k;
+  uint2* lists = reinterpret_cast<uint2*>(a.part);
+  float2* stats = reinterpret_cast<float2*>(reinterpret_cast<char*>(a.part) + a.list_stats);
+  const UnitPlan un = plan_unit(a, tail.u);
+  const int rows = unit_rows(a, un, UT);
+  const int32_t* ids = p.ids_base + (long long)un.seq * p.ids_stride + un.tile * kBM;
+  for (int r = tid; r < kBM * UT; r += kAThreadsL) gid_s[r] = r < rows ? __ldcg(ids + r) : -1;
+  const int tb = tail.e & 1;
+  mbar_wait(smem_u32(&tbars[2 * tb]), (tail.e >> 1) & 1);
+  tc_fence_after();
+  const int nh = (rows + kBM - 1) / kBM;
+  for (int h = 0; h < nh; ++h) {
+    const long long gt = (long long)un.seq * a.tps + un.tile + h;
+    if (warp < kLW) {  // TMEM -> Zt[node][row]
+      const int lg = warp & 3, cgp = warp >> 2;
+      const int r = lg * 32 + lane;
+      const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + tb * UT * NT + h * NT;
+      for (int c0 = cgp * 16; c0 < NT && c0 < p.n; c0 += 64) {
+        float v[16];
+        tmem_ld16(taddr + c0, v);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) Zt[(c0 + c) * kBM + r] = v[c];
+      }
+    }
+    __syncthreads();
+    int32_t gid[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) gid[j] = gid_s[h * kBM + lane + 32 * j];
+    for (int node = warp; node < p.n; node += kWarps)
+      warp_tile_topk(Zt + node * kBM, gid, k, cand + warp * kBM, lists + (gt * p.n + node) * k, stats + gt * p.n + node,
+                     p.logits ? p.logits + ((long long)un.seq * p.n + node) * a.dbg_ld + (un.tile + h) * kBM : nullptr);
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------------------ kernel A
-template <int NT, bool FUSED, int AG, int UT>
-__global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_constant__ SplitArgs a) {
-  using C = ACfg<NT, AG, UT>;
+template <int NT, bool FUSED, int AG, int UT, bool LIST = false>
+__global__ void __launch_bounds__(LIST ? kAThreadsL : kAThreads, 1) head_stream_kernel(const __grid_constant__ SplitArgs a) {
+  using C = ACfg<NT, AG, UT, LIST>;
   constexpr int kRows = kBM * UT;  // rows per unit
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStageArea);
   // bars[0..St) full, [St..2St) empty, [2St] tmem_full, [2St+1] tmem_empty
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::kStages + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::kStages + 4);
   __shared__ int32_t ids_s[2][kBM * UT];  // the unit's row ids (double-buffered: the next unit's are prefetched)
   __shared__ int sh_m[2];
+  __shared__ ListTail sh_tail;  // list mode: the CTA's last unit, left to the joint tail
 
   const HeadProblem& p = a.p;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -259,7 +506,11 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
       mbar_init(smem_u32(&bars[C::kStages + s]), 1);     // empty: one tcgen05.commit
     }
     mbar_init(smem_u32(&bars[2 * C::kStages]), 1);       // tmem_full
-    mbar_init(smem_u32(&bars[2 * C::kStages + 1]), kLW); // tmem_empty: one arrival per drain warp
+    mbar_init(smem_u32(&bars[2 * C::kStages + 1]), LIST ? kEW : kLW); // tmem_empty: one arrival per drain warp
+    if (LIST) {  // the second TMEM buffer's pair
+      mbar_init(smem_u32(&bars[2 * C::kStages + 2]), 1);
+      mbar_init(smem_u32(&bars[2 * C::kStages + 3]), kEW);
+    }
     fence_proxy_async();
   }
   if (warp == kLW) {
@@ -287,7 +538,14 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
   const uint32_t tmem = *tmem_slot;
   if (tid == 0) trace_mark(p.trace, 1);
 
-  if (FUSED && (int)blockIdx.x == a.heads) {
+  if (LIST && warp > kLW) {
+    // list mode: the epilogue warps (tmem_full / tmem_empty pairs: bars[2St], [2St+2] / [2St+1], [2St+3])
+    uint8_t* ex = smem + C::kStageArea + 256;
+    float* Z = reinterpret_cast<float*>(ex);
+    int32_t* gid_s = reinterpret_cast<int32_t*>(ex + kZCols * kBM * 4);
+    uint2* cand = reinterpret_cast<uint2*>(ex + kZCols * kBM * 4 + 2 * kBM * 4);
+    list_epilogue<NT, UT>(a, tmem, bars + 2 * C::kStages, Z, gid_s, cand, &sh_tail);
+  } else if (FUSED && (int)blockIdx.x == a.heads) {
     // the updater: a2 while every other CTA streams
     uint8_t* base = smem;
     UpdSmem& us = *reinterpret_cast<UpdSmem*>(base);
@@ -320,8 +578,13 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
         if (tid == kBM) sh_m[buf] = a.L - (un.tile - a.tps) * kBM;
       }
     };
+    // loaders + MMA warp (the list-mode epilogue warps run their own loop)
+    auto sync_lm = [] {
+      if (LIST) named_sync(1, kAThreads);
+      else __syncthreads();
+    };
     if ((int)blockIdx.x < a.units) fetch_ids(cur, 0);
-    __syncthreads();
+    sync_lm();
     if (tid == 0) trace_mark(p.trace, 7);
     if (tid == 0 && p.trace) p.trace[(long long)blockIdx.x * kTraceSlots + 12] = clock64();
     for (int u = blockIdx.x; u < a.units; u += stride, ++local) {
@@ -356,7 +619,7 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
           if (tid < kRows) ids_s[buf ^ 1][tid] = nx_id;
           if (tid == kRows) sh_m[buf ^ 1] = nx_m;
         }
-        __syncthreads();
+        sync_lm();
         continue;
       }
       const int kb0 = un.kb0, nk = un.nk;
@@ -418,6 +681,7 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
           }
         }
         if (tid == 0 && local == 0) trace_mark(p.trace, 3);
+        if (!LIST) {
         // ---------------- drain: TMEM -> the unit's partial tile in L2
         mbar_wait(smem_u32(&bars[2 * C::kStages]), nrun & 1);
         tc_fence_after();
@@ -443,9 +707,16 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&bars[2 * C::kStages + 1]));
+        }
       } else {
         // ---------------- MMA issue (warp 16, one lane)
-        if (nrun > 0) {  // the previous unit's partial has left TMEM
+        const int tb = LIST ? (nrun & 1) : 0;  // TMEM buffer (list mode: double-buffered)
+        if (LIST) {
+          if (nrun >= 2) {  // the epilogue has read this buffer's previous unit
+            mbar_wait(smem_u32(&bars[2 * C::kStages + 2 * tb + 1]), ((nrun >> 1) - 1) & 1);
+            tc_fence_after();
+          }
+        } else if (nrun > 0) {  // the previous unit's partial has left TMEM
           mbar_wait(smem_u32(&bars[2 * C::kStages + 1]), (nrun - 1) & 1);
           tc_fence_after();
         }
@@ -464,11 +735,14 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
                 for (int kk = 0; kk < kBK / 16; ++kk)
 #pragma unroll
                   for (int h = 0; h < UT; ++h)  // the UT tiles share the H operand
-                    umma_bf16(tmem + h * NT, sw128_desc(sA + at * C::kAtomA + h * (kBM * 128) + kk * 32),
+                    umma_bf16(tmem + (tb * UT + h) * NT, sw128_desc(sA + at * C::kAtomA + h * (kBM * 128) + kk * 32),
                               sw128_desc(sB + at * C::kAtomB + kk * 32), idesc, (q | at | kk) ? 1u : 0u);
               }
             umma_commit(smem_u32(&bars[C::kStages + stage]));
-            if (q == nst - 1) umma_commit(smem_u32(&bars[2 * C::kStages]));
+            if (q == nst - 1) {
+              umma_commit(smem_u32(&bars[2 * C::kStages + 2 * tb]));
+              if (LIST) trace_mark(p.trace, 4);  // list mode: the last unit's last MMA issued
+            }
           }
           __syncwarp();
         }
@@ -479,9 +753,20 @@ __global__ void __launch_bounds__(kAThreads, 1) head_stream_kernel(const __grid_
         if (tid < kRows) ids_s[buf ^ 1][tid] = nx_id;
         if (tid == kRows) sh_m[buf ^ 1] = nx_m;
       }
-      __syncthreads();  // ids_s[buf] free; the next unit's ids in ids_s[buf ^ 1]
+      sync_lm();  // ids_s[buf] free; the next unit's ids in ids_s[buf ^ 1]
     }
     if (FUSED && !arrived && tid == kLoaders) red_add_release(a.arrive_ctr, 1u);
+  }
+  if (LIST) {  // the joint tail: every warp reduces the CTA's last unit
+    __syncthreads();
+    const ListTail t = sh_tail;
+    if (t.u >= 0) {
+      uint8_t* ex = smem + C::kStageArea + 256;
+      if (tid == 0) trace_mark(p.trace, 5);
+      list_tail<NT, UT>(a, tmem, bars + 2 * C::kStages, reinterpret_cast<float*>(smem),
+                        reinterpret_cast<int32_t*>(ex + kZCols * kBM * 4), reinterpret_cast<uint2*>(ex), t);
+      if (tid == 0) trace_mark(p.trace, 6);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -855,6 +1140,254 @@ __global__ void __launch_bounds__(kBThreads, 1) head_select_kernel(const __grid_
   if (tid == 0 && p.trace) p.trace[(long long)(a.trace_base + blockIdx.x) * kTraceSlots + 15] = clock64();
 }
 
+// ------------------------------------------------------------------ kernel B, one round of <= 32 tiles
+// One CTA (32 warps) per (sequence, node), warp w on tile w (regular tiles
+// [0, tps), then patch tiles): the S partials of its lane's 4 rows summed in
+// K-chunk order (as head_select_kernel), then warp_topk4 -> the tile's top-k
+// list + (M, sum exp) in shared memory; warp 0 merges the <= 32 lists (the
+// k-th largest list head bounds every top-k key from below; the entries above
+// it are ranked by counting) and folds the lse.
+__global__ void __launch_bounds__(kBThreads, 1) head_select_tiles_kernel(const __grid_constant__ SplitArgs a) {
+  __shared__ uint2 lst[kBWarps][kMaxK];
+  __shared__ float2 sst[kBWarps];
+  __shared__ uint2 csw[kBWarps][kBM];  // per-warp candidate scratch, then the merge's candidates
+  uint2* cm = &csw[0][0];              // (free once every warp has its list)
+  const HeadProblem& p = a.p;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int k = a.k;
+  const int pair = blockIdx.x;
+  const int seq = pair / p.n, node = pair - seq * p.n;
+  const int ntp = a.tps + a.n_patch;
+  const long long pst = (long long)p.n * kBM;
+  const int r0 = 4 * lane;
+  const int tile = warp;
+  const bool on = tile < ntp;
+  int S = 0, base = 0;
+  warm_params(a);
+  if (on) {
+    tile_units(a, global_tile(a, seq, tile), S, base);
+    if (lane == 0) {
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.rowgid + ((long long)seq * ntp + tile) * kBM));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.part + (long long)base * pst + (long long)node * kBM));
+    }
+  }
+  if (tid == 0) trace_b(a, 0);
+  pdl_wait();  // A complete: partials, row ids (and the fused step's drop bitmap) visible
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (tid == 0) {
+    trace_b(a, 1);
+    if (p.trace) p.trace[(long long)(a.trace_base + blockIdx.x) * kTraceSlots + 12] = 0xB;  // a B row
+  }
+  if (on) {
+    const int4 g4 = __ldcg(reinterpret_cast<const int4*>(a.rowgid + ((long long)seq * ntp + tile) * kBM) + lane);
+    const uint32_t dw = a.drop ? __ldcg(&a.drop[tile * 4 + (lane >> 3)]) >> ((lane & 7) * 4) : 0u;
+    float zz[4] = {0.f, 0.f, 0.f, 0.f};
+    const float* src = a.part + (long long)base * pst + (long long)node * kBM + r0;
+    const int rot = tile % S;
+    for (int c0 = 0; c0 < S; c0 += 8) {  // K chunk c was computed by split (c - tile) mod S
+      float4 x[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (c0 + q < S) {
+          int sp = c0 + q - rot;
+          if (sp < 0) sp += S;
+          x[q] = __ldcg(reinterpret_cast<const float4*>(src + (long long)sp * pst));
+        }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (c0 + q < S) { zz[0] += x[q].x; zz[1] += x[q].y; zz[2] += x[q].z; zz[3] += x[q].w; }
+    }
+    const int32_t g[4] = {g4.x, g4.y, g4.z, g4.w};
+    uint32_t key[4];
+    int32_t gid[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const bool ok = g[i] >= 0 && !((dw >> i) & 1u);
+      key[i] = ok ? float_key(zz[i]) : 0u;
+      gid[i] = ok ? g[i] : -1;
+      if (g[i] >= 0 && p.logits) {
+        const long long col = tile < a.tps ? (long long)tile * kBM + r0 + i
+                                           : (long long)p.max_ids + (tile - a.tps) * kBM + r0 + i;
+        p.logits[((long long)seq * p.n + node) * a.dbg_ld + col] = zz[i];
+      }
+    }
+    if (tid == 0) trace_b(a, 5);
+    warp_topk4(key, gid, k, csw[warp], lst[warp], &sst[warp]);
+  }
+  __syncthreads();
+  if (tid == 0) trace_b(a, 7);
+  const bool has = lane < ntp;
+  if (warp == 1) {  // lse: fold the tiles' (M, sum exp)
+    float M = has ? sst[lane].x : -INFINITY, E = has ? sst[lane].y : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, M, o);
+      const float e2 = __shfl_xor_sync(0xffffffffu, E, o);
+      lse_fold(M, E, m2, e2);
+    }
+    if (a.lse && lane == 0) a.lse[(long long)seq * p.n + node] = M == -INFINITY ? -INFINITY : M + logf(E);
+  }
+  if (warp != 0) return;
+  // ---- merge the tiles' lists (lane t: tile t)
+  const uint32_t head = has ? lst[lane][0].x : 0u;
+  uint32_t v = head;
+#pragma unroll
+  for (int sz = 2; sz <= 32; sz <<= 1)
+#pragma unroll
+    for (int st = sz >> 1; st > 0; st >>= 1) {
+      const uint32_t o = __shfl_xor_sync(0xffffffffu, v, st);
+      const bool keep_min = ((lane & st) == 0) == ((lane & sz) == 0);
+      v = keep_min ? (o < v ? o : v) : (o > v ? o : v);
+    }
+  const uint32_t T = __shfl_sync(0xffffffffu, v, 32 - k);  // k distinct heads reach it (0: fewer than k tiles)
+  int c = 0;  // the list is sorted: the entries >= T are a prefix
+  if (has) {
+#pragma unroll 8
+    for (int q = 0; q < k; ++q) {
+      const uint32_t x = lst[lane][q].x;
+      c += (x != 0u && x >= T) ? 1 : 0;
+    }
+  }
+  int pre = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, pre, o);
+    if (lane >= o) pre += y;
+  }
+  const int cnt = __shfl_sync(0xffffffffu, pre, 31);
+  for (int q = 0; q < c; ++q) cm[pre - c + q] = lst[lane][q];
+  __syncwarp();
+  const long long ob = ((long long)seq * p.n + node) * k;
+  for (int q = lane; q < cnt; q += 32) {
+    const uint2 me = cm[q];
+    int rk = 0;
+#pragma unroll 4
+    for (int f = 0; f < cnt; ++f) {
+      const uint2 o = cm[f];
+      rk += key_before(o.x, o.y, me.x, me.y) ? 1 : 0;
+    }
+    if (rk < k) {
+      a.topk_logit[ob + rk] = key_value(me.x);
+      a.topk_id[ob + rk] = (int32_t)me.y;
+    }
+  }
+  for (int q = cnt + lane; q < k; q += 32) {
+    a.topk_logit[ob + q] = -INFINITY;
+    a.topk_id[ob + q] = -1;
+  }
+  if (tid == 0) trace_b(a, 4);
+}
+
+// ------------------------------------------------------------------ list-mode merge
+// One (sequence, node) pair per WPP warps (8 / WPP pairs per 256-thread CTA):
+// the exact top-k of the union of the pair's live tiles' top-k lists (a
+// global top-k entry is in its tile's list: fewer than k entries of that tile
+// precede it) and lse = fold of the tiles' (M, sum exp).  Threshold: the k-th
+// largest of the threads' maximum list heads -- k distinct heads reach it, so
+// every top-k entry does; the entries >= it (a few per pair) are ranked by
+// counting.
+constexpr int kMThreads = 256;
+template <int WPP>
+__global__ void __launch_bounds__(kMThreads) head_merge_kernel(const __grid_constant__ SplitArgs a) {
+  constexpr int PP = kMThreads / 32 / WPP;  // pairs per CTA
+  constexpr int PT = 32 * WPP;              // threads per pair
+  extern __shared__ __align__(16) uint2 mbuf[];
+  __shared__ int cnt_s[PP];
+  __shared__ uint32_t thr_s[kMThreads / 32];
+  __shared__ float2 lse_s[kMThreads / 32];
+  const HeadProblem& p = a.p;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int pi = warp / WPP, pt = tid - pi * PT;
+  const int k = a.k;
+  const int cap = a.tps * k;
+  uint2* cs = mbuf + (size_t)pi * cap;
+  const int pair = blockIdx.x * PP + pi;
+  const bool live = pair < p.batch * p.n;
+  const int seq = live ? pair / p.n : 0, node = live ? pair - seq * p.n : 0;
+  if (pt == 0) cnt_s[pi] = 0;
+  warm_params(a);
+  pdl_wait();  // the stream kernel complete: its lists visible
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int T = live ? (clamp_nact(p, seq) + kBM - 1) / kBM : 0;  // live tiles
+  const uint2* lists = reinterpret_cast<const uint2*>(a.part);
+  const float2* stats = reinterpret_cast<const float2*>(reinterpret_cast<const char*>(a.part) + a.list_stats);
+  const long long t0 = (long long)seq * a.tps;
+  float M = -INFINITY, E = 0.f;
+  uint32_t hm = 0u;
+#pragma unroll 4
+  for (int j = pt; j < T; j += PT) {
+    const long long ti = (t0 + j) * p.n + node;
+    const uint2 h0 = __ldcg(lists + ti * k);
+    const float2 st = __ldcg(stats + ti);
+    lse_fold(M, E, st.x, st.y);
+    hm = h0.x > hm ? h0.x : hm;
+  }
+  uint32_t thr = warp_kth_key(hm, k);
+  if (WPP > 1) {
+    if (lane == 0) thr_s[warp] = thr;
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < WPP; ++w) thr = thr_s[pi * WPP + w] > thr ? thr_s[pi * WPP + w] : thr;
+  } else {
+    __syncwarp();
+  }
+  // every list entry >= thr (lists are sorted: stop at the first below)
+  for (int j = pt; j < T; j += PT) {
+    const uint2* L = lists + ((t0 + j) * p.n + node) * k;
+    for (int e0 = 0; e0 < k; e0 += 8) {
+      uint2 c[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) c[q] = e0 + q < k ? __ldcg(L + e0 + q) : make_uint2(0u, 0u);
+      bool more = true;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (more && c[q].x != 0u && c[q].x >= thr) {
+          const int o = atomicAdd(&cnt_s[pi], 1);
+          cs[o] = c[q];
+        } else {
+          more = false;
+        }
+      }
+      if (!more) break;
+    }
+  }
+  if (WPP > 1) __syncthreads();
+  else __syncwarp();
+  const int cnt = cnt_s[pi];
+  const long long ob = ((long long)seq * p.n + node) * k;
+  if (live) {
+    for (int q = pt; q < cnt; q += PT) {
+      const uint2 me = cs[q];
+      int rk = 0;
+      for (int f = 0; f < cnt; ++f) {
+        const uint2 o = cs[f];
+        rk += key_before(o.x, o.y, me.x, me.y) ? 1 : 0;
+      }
+      if (rk < k) {
+        a.topk_logit[ob + rk] = key_value(me.x);
+        a.topk_id[ob + rk] = (int32_t)me.y;
+      }
+    }
+    for (int q = cnt + pt; q < k; q += PT) {
+      a.topk_logit[ob + q] = -INFINITY;
+      a.topk_id[ob + q] = -1;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, M, o);
+    const float e2 = __shfl_xor_sync(0xffffffffu, E, o);
+    lse_fold(M, E, m2, e2);
+  }
+  if (WPP > 1) {
+    if (lane == 0) lse_s[warp] = make_float2(M, E);
+    __syncthreads();
+    if (pt == 0)
+      for (int w = 1; w < WPP; ++w) lse_fold(M, E, lse_s[pi * WPP + w].x, lse_s[pi * WPP + w].y);
+  }
+  if (live && pt == 0 && a.lse) a.lse[(long long)seq * p.n + node] = M == -INFINITY ? -INFINITY : M + logf(E);
+}
+
 // ------------------------------------------------------------------ host side
 struct SplitLayout {
   size_t part, rowgid, arrive, mrows, drop, total;
@@ -883,7 +1416,8 @@ int num_sms_cached() { return g_num_sms; }
 int g_stream_only = 0;  // debug mode 1: kernel A alone (measurement; no outputs are written)
 // experiments (NANOSPEC_SPLIT_FLAGS): 1 = skip kernel B, 2 = no PDL, 16 = kernel B alone,
 // 32 = one K atom per pipeline stage, 64 = no 256-row units in the persistent mode,
-// 128 = one K atom per stage with 256-row units
+// 128 = one K atom per stage with 256-row units, 256 = no list mode (split-K 1: partial tiles + select kernel),
+// 512 = the radix select kernel for one-round heads (instead of per-tile warp lists)
 int g_split_flags = -1;
 int split_flags() {
   if (g_split_flags < 0) {
@@ -927,14 +1461,15 @@ cudaError_t launch_ex(K kern, dim3 grid, int threads, size_t smem, cudaStream_t 
   return e;
 }
 
-template <int NT, bool FUSED, int AG, int UT>
+template <int NT, bool FUSED, int AG, int UT, bool LIST = false>
 cudaError_t set_attr_once() {
   static bool done[64] = {false};  // per device: the attribute is per (function, device)
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
   if (done[dev]) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(head_stream_kernel<NT, FUSED, AG, UT>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, ACfg<NT, AG, UT>::kSmemBytes);
+  cudaError_t e = cudaFuncSetAttribute(head_stream_kernel<NT, FUSED, AG, UT, LIST>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       ACfg<NT, AG, UT, LIST>::kSmemBytes);
   if (e == cudaSuccess) done[dev] = true;
   return e;
 }
@@ -960,6 +1495,8 @@ cudaError_t launch_select_cfg(const SplitArgs& b, cudaStream_t stream) {
 cudaError_t launch_select(const SplitArgs& b, int num_sms, cudaStream_t stream) {
   const int pairs = b.p.batch * b.p.n;
   const int ntp = b.tps + b.n_patch;
+  if (ntp <= kBWarps && !(split_flags() & 512))  // one round: per-tile warp lists, then a warp merge
+    return launch_ex(head_select_tiles_kernel, dim3(pairs), kBThreads, 0, stream, b);
   if (pairs >= 4 * num_sms && ntp <= BCfg<4, 3>::kRound && b.S == 1 && b.extra == 0)
     return launch_select_cfg<4, 3, false>(b, stream);
   if (ntp > BCfg<1, 1>::kRound) return launch_select_cfg<1, 1, true>(b, stream);
@@ -1003,6 +1540,51 @@ cudaError_t launch_nt_ut2_ag(const SplitArgs& a, int grid_a, cudaStream_t stream
 cudaError_t launch_nt_ut2(const SplitArgs& a, int grid_a, cudaStream_t stream) {
   if (split_flags() & 128) return launch_nt_ut2_ag<1>(a, grid_a, stream);  // experiment: 1 atom per stage
   return launch_nt_ut2_ag<2>(a, grid_a, stream);  // 2 atoms x 2 tiles per stage, two stages in flight
+}
+
+// List mode: the stream kernel with epilogue warps, then the merge kernel.
+template <int WPP>
+cudaError_t launch_merge_cfg(const SplitArgs& b, cudaStream_t stream) {
+  static bool done[64] = {false};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  constexpr int PP = kMThreads / 32 / WPP;
+  if (!done[dev]) {
+    const cudaError_t e = cudaFuncSetAttribute(head_merge_kernel<WPP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               WPP == 1 ? PP * 32 * kMaxK * 8 : kListCap * 8);
+    if (e != cudaSuccess) return e;
+    done[dev] = true;
+  }
+  const int pairs = b.p.batch * b.p.n;
+  const size_t smem = (size_t)PP * b.tps * b.k * 8;
+  return launch_ex(head_merge_kernel<WPP>, dim3((pairs + PP - 1) / PP), kMThreads, smem, stream, b);
+}
+
+template <int NT, int AG, int UT>
+cudaError_t launch_list_pair(const SplitArgs& a, int grid_a, cudaStream_t stream) {
+  cudaError_t e = set_attr_once<NT, false, AG, UT, true>();
+  if (e != cudaSuccess) return e;
+  e = launch_ex(head_stream_kernel<NT, false, AG, UT, true>, dim3(grid_a), kAThreadsL,
+                ACfg<NT, AG, UT, true>::kSmemBytes, stream, a);
+  if (e != cudaSuccess || (split_flags() & 1) || g_stream_only) return e;
+  SplitArgs b = a;
+  b.trace_base = grid_a;
+  return a.tps <= 32 ? launch_merge_cfg<1>(b, stream) : launch_merge_cfg<8>(b, stream);
+}
+
+cudaError_t launch_list(const SplitArgs& a, int grid_a, cudaStream_t stream) {
+  const int n = a.p.n;
+  if (a.ut == 2) {
+    if (n <= 16) return launch_list_pair<16, 2, 2>(a, grid_a, stream);
+    if (n <= 32) return launch_list_pair<32, 2, 2>(a, grid_a, stream);
+    if (n <= 64) return launch_list_pair<64, 2, 2>(a, grid_a, stream);
+    return launch_list_pair<128, 1, 2>(a, grid_a, stream);
+  }
+  if (n <= 16) return launch_list_pair<16, 2, 1>(a, grid_a, stream);
+  if (n <= 32) return launch_list_pair<32, 2, 1>(a, grid_a, stream);
+  if (n <= 64) return launch_list_pair<64, 2, 1>(a, grid_a, stream);
+  if (n <= 128) return launch_list_pair<128, 2, 1>(a, grid_a, stream);
+  return launch_list_pair<256, 1, 1>(a, grid_a, stream);
 }
 
 // atoms per stage: 2 (256 contiguous bytes of a row per stage) unless the
@@ -1081,6 +1663,12 @@ cudaError_t launch_head_tc(const HeadProblem& p, int k, float* topk_logit, int32
     a.units = p.batch * a.upt;
   }
   a.heads = a.units < G ? a.units : G;
+  // more tiles than SMs (split-K 1, persistent): the tiles are reduced to
+  // top-k lists inside the stream kernel and merged by a small kernel
+  if (a.S == 1 && a.extra == 0 && a.ntiles > G && (long long)a.tps * k <= kListCap && !(split_flags() & 256)) {
+    a.list_stats = ((long long)a.ntiles * p.n * k * 8 + 255) / 256 * 256;
+    return launch_list(a, a.heads, stream);
+  }
   return launch_nt<false>(a, a.heads, stream);
 }
 

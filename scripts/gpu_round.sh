@@ -22,6 +22,6 @@ cut -c1-400 gpurun_out/${T}_bench_vp32k.json
 timeout 600 python bench.py --config qwen512 2>&1 | tail -1 > gpurun_out/${T}_bench_qwen512.json
 cut -c1-600 gpurun_out/${T}_bench_qwen512.json
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"head_stream_kernel" -s 20 -c 1 -o gpurun_out/${T}_stream_full python bench.py --steps 10 --warmup 5 --no-cpu --no-dense --replays 1 > gpurun_out/${T}_ncu_full.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"head_select_kernel" -s 20 -c 1 -o gpurun_out/${T}_select_full python bench.py --steps 10 --warmup 5 --no-cpu --no-dense --replays 1 > gpurun_out/${T}_ncu_full2.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"head_select" -s 20 -c 1 -o gpurun_out/${T}_select_full python bench.py --steps 10 --warmup 5 --no-cpu --no-dense --replays 1 > gpurun_out/${T}_ncu_full2.log 2>&1
 tail -n 1 gpurun_out/${T}_ncu_full.log gpurun_out/${T}_ncu_full2.log
 cp profiles/traffic.json gpurun_out/${T}_traffic.json

@@ -24,7 +24,7 @@ def main():
     per = defaultdict(lambda: defaultdict(list))  # kernel -> metric -> values
     for r in rows:
         name = r.get("Kernel Name", "")
-        short = "stream" if "head_stream_kernel" in name else "select" if "head_select_kernel" in name else \
+        short = "stream" if "head_stream_kernel" in name else "select" if "head_select" in name or "head_merge" in name else \
             "update" if "state_update" in name else name[:40]
         val = float(str(r.get("Metric Value", "0")).replace(",", ""))
         unit = r.get("Metric Unit", "")
