@@ -248,8 +248,8 @@ def run_ours(args):
     R = max(1, min(R, V // pool))
     W = SI.bf16_weights(V, d, seed=0, device=dev)
     pools = SI.disjoint_pools(V, pool, R, seed=3 + rank)
-    # step, two-launch step, update-only, e2e, repack variant
-    total_steps_per_seq = (args.warmup + 5 * args.steps + 2 * R) // R + 8
+    # step, two-launch step, update-only, e2e (serial, pipelined), repack variant
+    total_steps_per_seq = (args.warmup + 6 * args.steps + 2 * R) // R + 8
     states, outs, upd_d, upd_v = [], [], [], []
     Hs = SI.bf16_hidden(n, d, seed=1 + rank, device=dev, batch=R)
     for r in range(R):
@@ -494,7 +494,28 @@ def run_ours(args):
         P.step_host(states[r], 0, io, blk, W, k)
     ev1.record(stream)
     torch.cuda.synchronize()
+    us_e2e_serial = ev0.elapsed_time(ev1) * 1e3 / E
+    # the same through nanospec_step_host_async (two staging slots): each step's
+    # input copy runs on a copy stream while the previous step (another
+    # sequence) computes; every step still copies its inputs in and its
+    # results out inside the timed region
+    iop = P.StepHostIO(n, d, 60, 3, k, Wm, dev, slots=2)
+    blocks = []
+    for s_ in range(E):
+        r = s_ % R
+        c = cursor[r] + s_ // R
+        blocks.append((r, iop.pack_inputs(Hs[r], upd_d[r][c], upd_v[r][c])))
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    iop.copy_stream.wait_event(ev0)
+    for s_ in range(E):
+        r, blk = blocks[s_]
+        cursor[r] += 1
+        P.step_host(states[r], 0, iop, blk, W, k)
+    ev1.record(stream)
+    torch.cuda.synchronize()
     us_e2e = ev0.elapsed_time(ev1) * 1e3 / E
+    extra["us_e2e_serial_host_step"] = round(us_e2e_serial, 3)
     assert all(st.read(0)["n_active"] == Wm for st in states)
     h2d = n * d * 2 + 63 * 4
     d2h = n * k * 8 + n * 4

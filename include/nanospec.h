@@ -263,6 +263,21 @@ nanospec_status nanospec_step_host(nanospec_state st, int32_t seq, const void* h
                                    void* h_out, void* d_io, size_t io_bytes, void* d_scratch, size_t scratch_bytes,
                                    cudaStream_t stream);
 
+/* nanospec_step_host for a pipeline of steps: the host->device copy runs on
+ * `copy_stream` (it overlaps the previous step's kernels), the step and the
+ * device->host copy on `stream`, ordered by two caller-created events.  A
+ * caller alternates >= 2 staging slots (d_io, h_out, ev_in, ev_done each):
+ * the copy into a slot first waits for ev_done, recorded by the previous step
+ * that used the slot (an event never recorded means no wait); the step waits
+ * for ev_in.  Results of a step are in its h_out once its ev_done completes.
+ * Same layouts and results as nanospec_step_host; EINVAL on bad arguments or
+ * copy_stream == stream, ECUDA on a failed copy / event call. */
+nanospec_status nanospec_step_host_async(nanospec_state st, int32_t seq, const void* h_in, int32_t n_draft,
+                                         int32_t k_ver, const void* d_w_head, int32_t d_model, int64_t ldw,
+                                         int32_t n_nodes, int32_t k, void* h_out, void* d_io, size_t io_bytes,
+                                         void* d_scratch, size_t scratch_bytes, cudaStream_t stream,
+                                         cudaStream_t copy_stream, cudaEvent_t ev_in, cudaEvent_t ev_done);
+
 /* 1 if nanospec_step with these sizes runs fused (the update inside the head's
  * stream kernel) on the current device, 0 if it runs as update + head (same
  * results).  Host-only query. */

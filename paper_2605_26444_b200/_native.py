@@ -23,7 +23,7 @@ EXPORTS = [
     "nanospec_head_scratch_bytes", "nanospec_draft_logits_topk", "nanospec_draft_logits_topk_ex",
     "nanospec_logits_topk_ids", "nanospec_merge_topk", "nanospec_debug_set_trace",
     "nanospec_debug_set_head_mode", "nanospec_step", "nanospec_step_fused", "nanospec_step_debug",
-    "nanospec_step_host", "nanospec_step_host_io_bytes", "nanospec_tree_expand", "nanospec_tree_rerank",
+    "nanospec_step_host", "nanospec_step_host_async", "nanospec_step_host_io_bytes", "nanospec_tree_expand", "nanospec_tree_rerank",
     "nanospec_repack", "nanospec_draft_logits_topk_packed",
 ]
 
@@ -75,6 +75,8 @@ def lib():
     L.nanospec_step_host_io_bytes.argtypes = [i32, i32, i32, i32, i32, ctypes.POINTER(sz), ctypes.POINTER(sz)]
     L.nanospec_step_host_io_bytes.restype = sz
     L.nanospec_step_host.argtypes = [vp, i32, vp, i32, i32, vp, i32, i64, i32, i32, vp, vp, sz, vp, sz, vp]
+    L.nanospec_step_host_async.argtypes = [vp, i32, vp, i32, i32, vp, i32, i64, i32, i32, vp, vp, sz, vp, sz, vp, vp,
+                                           vp, vp]
     L.nanospec_step_fused.argtypes = [vp, i32, i32, i32, i32, i32]
     L.nanospec_step.argtypes = [vp, i32, vp, i32, vp, i32, vp, i32, i64, vp, i32, i32, vp, vp, vp, vp, sz, vp]
     L.nanospec_repack.argtypes = [vp, i32, vp, i32, i64, vp, i64, vp, vp]

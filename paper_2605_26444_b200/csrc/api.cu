@@ -397,6 +397,38 @@ nanospec_status nanospec_step_host(nanospec_state st, int32_t seq, const void* h
   return cuda_status(cudaMemcpyAsync(h_out, dout, out_used, cudaMemcpyDeviceToHost, stream));
 }
 
+nanospec_status nanospec_step_host_async(nanospec_state st, int32_t seq, const void* h_in, int32_t n_draft,
+                                         int32_t k_ver, const void* d_w_head, int32_t d_model, int64_t ldw,
+                                         int32_t n_nodes, int32_t k, void* h_out, void* d_io, size_t io_bytes,
+                                         void* d_scratch, size_t scratch_bytes, cudaStream_t stream,
+                                         cudaStream_t copy_stream, cudaEvent_t ev_in, cudaEvent_t ev_done) {
+  if (!h_in || !h_out || !d_io || !ev_in || !ev_done || copy_stream == stream) return NANOSPEC_EINVAL;
+  size_t ib = 0, ob = 0;
+  if (nanospec_step_host_io_bytes(n_nodes, d_model, n_draft, k_ver, k, &ib, &ob) == 0 || io_bytes < ib + ob)
+    return NANOSPEC_EINVAL;
+  char* din = (char*)d_io;
+  char* dout = din + ib;
+  const size_t hb = (size_t)n_nodes * d_model * 2;
+  const size_t in_used = hb + (size_t)(n_draft + k_ver) * 4;
+  const size_t out_used = (size_t)n_nodes * k * 8 + (size_t)n_nodes * 4;
+  // the previous step that used this staging slot (and h_out) is complete
+  // before the copy overwrites it (an event never recorded: no wait)
+  if (cudaStreamWaitEvent(copy_stream, ev_done, 0) != cudaSuccess) return NANOSPEC_ECUDA;
+  if (cudaMemcpyAsync(din, h_in, in_used, cudaMemcpyHostToDevice, copy_stream) != cudaSuccess) return NANOSPEC_ECUDA;
+  if (cudaEventRecord(ev_in, copy_stream) != cudaSuccess) return NANOSPEC_ECUDA;
+  if (cudaStreamWaitEvent(stream, ev_in, 0) != cudaSuccess) return NANOSPEC_ECUDA;
+  const int32_t* dd = n_draft > 0 ? (const int32_t*)(din + hb) : nullptr;
+  const int32_t* dv = k_ver > 0 ? (const int32_t*)(din + hb) + n_draft : nullptr;
+  float* ol = (float*)dout;
+  int32_t* oi = (int32_t*)(dout + (size_t)n_nodes * k * 4);
+  float* os = (float*)(dout + (size_t)n_nodes * k * 8);
+  nanospec_status r = nanospec_step(st, seq, dd, n_draft, dv, k_ver, d_w_head, d_model, ldw, din, n_nodes, k, ol, oi,
+                                    os, d_scratch, scratch_bytes, stream);
+  if (r != NANOSPEC_OK) return r;
+  if (cudaMemcpyAsync(h_out, dout, out_used, cudaMemcpyDeviceToHost, stream) != cudaSuccess) return NANOSPEC_ECUDA;
+  return cuda_status(cudaEventRecord(ev_done, stream));
+}
+
 int32_t nanospec_step_fused(const nanospec_state st, int32_t n_draft, int32_t k_ver, int32_t d_model,
                             int32_t n_nodes, int32_t k) {
   if (!st || n_draft < 0 || k_ver < 0 || d_model <= 0 || d_model % 8 != 0) return 0;

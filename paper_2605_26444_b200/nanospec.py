@@ -250,7 +250,11 @@ class StepHostIO:
     in  = [hidden bf16 n x d][draft int32 n_draft][verify int32 k_ver],
     out = [topk_logit fp32 n x k][topk_id int32 n x k][lse fp32 n]."""
 
-    def __init__(self, n_nodes: int, d_model: int, n_draft: int, k_ver: int, k: int, w_max: int, device):
+    def __init__(self, n_nodes: int, d_model: int, n_draft: int, k_ver: int, k: int, w_max: int, device,
+                 slots: int = 1):
+        """slots >= 2: a pipeline (nanospec_step_host_async) -- each step's input
+        copy runs on a copy stream while the previous step computes; the slots'
+        staging, host results and events alternate."""
         ib, ob = ctypes.c_size_t(0), ctypes.c_size_t(0)
         total = N.lib().nanospec_step_host_io_bytes(n_nodes, d_model, n_draft, k_ver, k, ctypes.byref(ib),
                                                     ctypes.byref(ob))
@@ -258,9 +262,21 @@ class StepHostIO:
             raise N.NanoSpecError(N.EINVAL, "nanospec_step_host_io_bytes")
         self.n, self.d, self.n_draft, self.k_ver, self.k = n_nodes, d_model, n_draft, k_ver, k
         self.in_bytes, self.out_bytes = ib.value, ob.value
-        self.d_io = torch.empty(total, dtype=torch.uint8, device=device)
+        self.slots = slots
+        self.total = total
+        self.d_ios = [torch.empty(total, dtype=torch.uint8, device=device) for _ in range(slots)]
+        self.d_io = self.d_ios[0]
         self.scratch = HeadOutputs(1, n_nodes, k, w_max, device).scratch
-        self.h_out = torch.empty(self.out_bytes, dtype=torch.uint8).pin_memory()
+        self.h_outs = [torch.empty(self.out_bytes, dtype=torch.uint8).pin_memory() for _ in range(slots)]
+        self.h_out = self.h_outs[0]
+        self.slot = 0  # the slot of the most recent step
+        if slots > 1:
+            self.copy_stream = torch.cuda.Stream(device)
+            self.ev_in = [torch.cuda.Event() for _ in range(slots)]
+            self.ev_done = [torch.cuda.Event() for _ in range(slots)]
+            for e in self.ev_in + self.ev_done:  # create the events (torch creates them lazily)
+                e.record(self.copy_stream)
+            torch.cuda.current_stream(device).wait_stream(self.copy_stream)
         # input blocks handed to nanospec_step_host stay referenced until the
         # stream has consumed them (the library's cudaMemcpyAsync is invisible
         # to torch's pinned-memory allocator, which could otherwise recycle them)
@@ -280,23 +296,35 @@ class StepHostIO:
             torch.as_tensor(verify, dtype=torch.int32).cpu())
         return blk
 
-    def results(self):
-        """(topk_logit [n,k], topk_id [n,k], lse [n]) views of the host result block."""
+    def results(self, slot: int | None = None):
+        """(topk_logit [n,k], topk_id [n,k], lse [n]) views of a host result block
+        (default: the most recent step's; a pipeline's step is complete once
+        its ev_done event is)."""
         nk = self.n * self.k
-        return (self.h_out[:4 * nk].view(torch.float32).view(self.n, self.k),
-                self.h_out[4 * nk:8 * nk].view(torch.int32).view(self.n, self.k),
-                self.h_out[8 * nk:8 * nk + 4 * self.n].view(torch.float32))
+        h = self.h_outs[self.slot if slot is None else slot]
+        return (h[:4 * nk].view(torch.float32).view(self.n, self.k),
+                h[4 * nk:8 * nk].view(torch.int32).view(self.n, self.k),
+                h[8 * nk:8 * nk + 4 * self.n].view(torch.float32))
 
 
 def step_host(state: ActiveVocab, seq: int, io: StepHostIO, h_in: torch.Tensor, w_head: torch.Tensor, k: int):
     """nanospec_step_host: H2D of the packed inputs, the step, D2H of the packed
     results, asynchronous on the current stream (results in io.results() after a sync)."""
     _need(w_head, torch.bfloat16, "w_head")
-    st = N.lib().nanospec_step_host(
-        state.handle, seq, h_in.data_ptr(), io.n_draft, io.k_ver, _ptr(w_head), io.d, w_head.stride(0), io.n, k,
-        io.h_out.data_ptr(), _ptr(io.d_io), io.d_io.numel(), _ptr(io.scratch), io.scratch.numel(),
-        _stream(w_head.device))
-    N.check(st, "nanospec_step_host")
+    if io.slots > 1:  # pipelined: the input copy on io.copy_stream, slots alternate
+        sl = (io.slot + 1) % io.slots
+        st = N.lib().nanospec_step_host_async(
+            state.handle, seq, h_in.data_ptr(), io.n_draft, io.k_ver, _ptr(w_head), io.d, w_head.stride(0), io.n, k,
+            io.h_outs[sl].data_ptr(), _ptr(io.d_ios[sl]), io.total, _ptr(io.scratch), io.scratch.numel(),
+            _stream(w_head.device), io.copy_stream.cuda_stream, io.ev_in[sl].cuda_event, io.ev_done[sl].cuda_event)
+        N.check(st, "nanospec_step_host_async")
+        io.slot = sl
+    else:
+        st = N.lib().nanospec_step_host(
+            state.handle, seq, h_in.data_ptr(), io.n_draft, io.k_ver, _ptr(w_head), io.d, w_head.stride(0), io.n, k,
+            io.h_out.data_ptr(), _ptr(io.d_io), io.d_io.numel(), _ptr(io.scratch), io.scratch.numel(),
+            _stream(w_head.device))
+        N.check(st, "nanospec_step_host")
     ev = torch.cuda.Event()
     ev.record(torch.cuda.current_stream(w_head.device))
     io._inflight.append((ev, h_in))

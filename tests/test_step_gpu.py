@@ -224,6 +224,40 @@ def test_step_host_buffers(cuda_ok, llama):
         _check_head(v.unsqueeze(0), i.unsqueeze(0), l.unsqueeze(0), ids, Wb, H, k, f"host step {s}")
 
 
+def test_step_host_pipelined(cuda_ok, llama):
+    """nanospec_step_host_async (2 slots, input copies on a copy stream): four
+    steps issued back to back without a sync, then every step's results (read
+    from its slot once its event completed) and the final state equal the
+    oracle's."""
+    from paper_2605_26444_b200 import ActiveVocab, StepHostIO, step_host
+    W, Wb = llama
+    V, d = W.shape
+    Wm, n, k = 3072, 60, 10
+    pool = SI.disjoint_pools(V, Wm + 126, 1, seed=22)[0]
+    prompt, ups = SI.cyclic_fresh_updates(pool, Wm, 4)
+    st = ActiveVocab(V, Wm)
+    st.init(0, _t(prompt))
+    ref = O.OracleStream(V, Wm).init(prompt)
+    io = StepHostIO(n, d, 60, 3, k, Wm, "cuda", slots=2)
+    Hs = [SI.bf16_hidden(n, d, seed=700 + s, device="cuda") for s in range(len(ups))]
+    blocks = [io.pack_inputs(Hs[s], dd, vv) for s, (dd, vv) in enumerate(ups)]
+    torch.cuda.synchronize()
+    got = []
+    for s in range(len(ups)):
+        step_host(st, 0, io, blocks[s], W, k)
+        if s >= 1:  # the previous step's slot is reused two steps later: read it now
+            io.ev_done[1 - io.slot].synchronize()
+            got.append([x.clone() for x in io.results(1 - io.slot)])
+    torch.cuda.synchronize()
+    got.append([x.clone() for x in io.results()])
+    for s, (dd, vv) in enumerate(ups):
+        ref.update(dd, vv)
+        ids = ref.active()[0]
+        v, i, l = got[s]
+        _check_head(v.unsqueeze(0), i.unsqueeze(0), l.unsqueeze(0), ids, Wb, Hs[s], k, f"pipelined step {s}")
+    _check_state(st, ref, "pipelined host steps")
+
+
 def test_step_qwen_shape(cuda_ok):
     """configs[2] shape (V = 152064, d = 3584): a 2k-token prompt with K_pre = 3,
     then fused steps on the natural active set."""
