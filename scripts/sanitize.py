@@ -1,7 +1,8 @@
 """A tiny end-to-end pass of every kernel of the path, for compute-sanitizer
 (memcheck / synccheck / racecheck / initcheck): state init + update (fast and
 general paths, rule R2), the CUDA-core head + select, the tensor-core head
-(stream + select kernels; split-K > 1 and persistent), the fused step, the
+(stream + select kernels; split-K > 1, persistent, list mode + merge), the
+fused step (device and pipelined host buffers), the
 vocab-parallel merge, the draft-tree expansion / rerank and the repack variant.
 
     compute-sanitizer --tool memcheck python scripts/sanitize.py
@@ -47,6 +48,18 @@ def main():
     for b in range(3):
         stb.init(b, t(prompt[: 100 + 50 * b]))
     P.draft_logits_topk(stb, W, SI.bf16_hidden(n, d, seed=3, device="cuda", batch=3), k)
+    # list mode (more tiles than SMs, split-K 1): the dense head over [0, V2),
+    # 313 tiles -> 148 tile-pair units + 17 single-tile units, lists + merge
+    V2 = 40000
+    W2 = SI.bf16_weights(V2, d, seed=9, device="cuda")
+    allids = torch.arange(V2, dtype=torch.int32, device="cuda")
+    P.logits_topk_ids(allids, torch.tensor([V2], dtype=torch.int32, device="cuda"), W2,
+                      SI.bf16_hidden(n, d, seed=10, device="cuda"), k, debug_logits=True)
+    # host-buffer steps, pipelined (copy stream + two staging slots)
+    io = P.StepHostIO(n, d, 8, 3, k, 1024, "cuda", slots=2)
+    for dd, vv in SI.decode_steps(z, 9, 3, n_draft=8, k_ver=3):
+        P.step_host(st, 0, io, io.pack_inputs(SI.bf16_hidden(n, d, seed=11, device="cuda"), dd, vv), W, k)
+    torch.cuda.synchronize()
     # vocab-parallel merge of two shards
     v, i, l, _ = P.draft_logits_topk(st, W, SI.bf16_hidden(n, d, seed=4, device="cuda").reshape(1, n, d), k)
     P.merge_topk(torch.stack([v[0], v[0]]), torch.stack([i[0], i[0]]), torch.stack([l[0], l[0]]), k)
