@@ -352,7 +352,9 @@ struct ListTail {
 // for its TMEM buffer, stage each 64-node chunk of each 128-row tile into
 // shared memory (node-major), release the buffer after its last read, and
 // reduce every (tile, node) with warp_tile_topk into
-//   list[tile][node][0, k), stats[tile][node].
+//   list[seq][node][tile][0, k), stats[seq][node][tile] (a (sequence, node)
+//   pair's lists are contiguous: the merge reads them coalesced, from HBM when
+//   the weight stream has evicted them from L2).
 // The CTA's last unit is left to the joint tail (every warp of the CTA, once
 // the loaders and the MMA warp are done): its epilogue is the exposed part.
 template <int NT, int UT>
@@ -397,7 +399,7 @@ __device__ __forceinline__ void list_epilogue(const SplitArgs& a, uint32_t tmem,
     const int nh = (rows + kBM - 1) / kBM;
     const int ncc = (p.n + kZCols - 1) / kZCols;
     for (int h = 0; h < nh; ++h) {
-      const long long gt = (long long)un.seq * a.tps + un.tile + h;  // global tile
+      const long long gt = (long long)un.seq * p.n * a.tps + un.tile + h;  // + node * tps: the (tile, node) slot
       for (int cc = 0; cc < ncc; ++cc) {
         const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + tb * UT * NT + h * NT + cc * kZCols;
         const int r = lg * 32 + lane;
@@ -422,7 +424,7 @@ __device__ __forceinline__ void list_epilogue(const SplitArgs& a, uint32_t tmem,
         const int cn = min(kZCols, p.n - cc * kZCols);
         for (int c = ew; c < cn; c += kEW) {
           const int node = cc * kZCols + c;
-          warp_tile_topk(Z + c * kBM, gid, k, cs, lists + (gt * p.n + node) * k, stats + gt * p.n + node,
+          warp_tile_topk(Z + c * kBM, gid, k, cs, lists + (gt + (long long)node * a.tps) * k, stats + gt + (long long)node * a.tps,
                          p.logits ? p.logits + ((long long)un.seq * p.n + node) * a.dbg_ld + (un.tile + h) * kBM
                                   : nullptr);
         }
@@ -458,7 +460,7 @@ __device__ __forceinline__ void list_tail(const SplitArgs& a, uint32_t tmem, uin
   tc_fence_after();
   const int nh = (rows + kBM - 1) / kBM;
   for (int h = 0; h < nh; ++h) {
-    const long long gt = (long long)un.seq * a.tps + un.tile + h;
+    const long long gt = (long long)un.seq * p.n * a.tps + un.tile + h;
     if (warp < kLW) {  // TMEM -> Zt[node][row]
       const int lg = warp & 3, cgp = warp >> 2;
       const int r = lg * 32 + lane;
@@ -475,7 +477,8 @@ __device__ __forceinline__ void list_tail(const SplitArgs& a, uint32_t tmem, uin
 #pragma unroll
     for (int j = 0; j < 4; ++j) gid[j] = gid_s[h * kBM + lane + 32 * j];
     for (int node = warp; node < p.n; node += kWarps)
-      warp_tile_topk(Zt + node * kBM, gid, k, cand + warp * kBM, lists + (gt * p.n + node) * k, stats + gt * p.n + node,
+      warp_tile_topk(Zt + node * kBM, gid, k, cand + warp * kBM, lists + (gt + (long long)node * a.tps) * k,
+                     stats + gt + (long long)node * a.tps,
                      p.logits ? p.logits + ((long long)un.seq * p.n + node) * a.dbg_ld + (un.tile + h) * kBM : nullptr);
     __syncthreads();
   }
@@ -1306,22 +1309,28 @@ __global__ void __launch_bounds__(kMThreads) head_merge_kernel(const __grid_cons
   const int seq = live ? pair / p.n : 0, node = live ? pair - seq * p.n : 0;
   if (pt == 0) cnt_s[pi] = 0;
   warm_params(a);
+  if (tid == 0) trace_b(a, 0);
   pdl_wait();  // the stream kernel complete: its lists visible
   asm volatile("griddepcontrol.launch_dependents;");
+  if (tid == 0) {
+    trace_b(a, 1);
+    if (a.p.trace) a.p.trace[(long long)(a.trace_base + blockIdx.x) * kTraceSlots + 12] = 0xB;  // a B row
+  }
   const int T = live ? (clamp_nact(p, seq) + kBM - 1) / kBM : 0;  // live tiles
   const uint2* lists = reinterpret_cast<const uint2*>(a.part);
   const float2* stats = reinterpret_cast<const float2*>(reinterpret_cast<const char*>(a.part) + a.list_stats);
-  const long long t0 = (long long)seq * a.tps;
+  const long long t0 = ((long long)seq * p.n + node) * a.tps;  // the pair's tiles are contiguous
   float M = -INFINITY, E = 0.f;
   uint32_t hm = 0u;
 #pragma unroll 4
   for (int j = pt; j < T; j += PT) {
-    const long long ti = (t0 + j) * p.n + node;
+    const long long ti = t0 + j;
     const uint2 h0 = __ldcg(lists + ti * k);
     const float2 st = __ldcg(stats + ti);
     lse_fold(M, E, st.x, st.y);
     hm = h0.x > hm ? h0.x : hm;
   }
+  if (tid == 0) trace_b(a, 5);
   uint32_t thr = warp_kth_key(hm, k);
   if (WPP > 1) {
     if (lane == 0) thr_s[warp] = thr;
@@ -1333,7 +1342,7 @@ __global__ void __launch_bounds__(kMThreads) head_merge_kernel(const __grid_cons
   }
   // every list entry >= thr (lists are sorted: stop at the first below)
   for (int j = pt; j < T; j += PT) {
-    const uint2* L = lists + ((t0 + j) * p.n + node) * k;
+    const uint2* L = lists + (t0 + j) * k;
     for (int e0 = 0; e0 < k; e0 += 8) {
       uint2 c[8];
 #pragma unroll
@@ -1354,6 +1363,7 @@ __global__ void __launch_bounds__(kMThreads) head_merge_kernel(const __grid_cons
   if (WPP > 1) __syncthreads();
   else __syncwarp();
   const int cnt = cnt_s[pi];
+  if (tid == 0) trace_b(a, 7);
   const long long ob = ((long long)seq * p.n + node) * k;
   if (live) {
     for (int q = pt; q < cnt; q += PT) {
@@ -1386,6 +1396,7 @@ __global__ void __launch_bounds__(kMThreads) head_merge_kernel(const __grid_cons
       for (int w = 1; w < WPP; ++w) lse_fold(M, E, lse_s[pi * WPP + w].x, lse_s[pi * WPP + w].y);
   }
   if (live && pt == 0 && a.lse) a.lse[(long long)seq * p.n + node] = M == -INFINITY ? -INFINITY : M + logf(E);
+  if (tid == 0) trace_b(a, 4);
 }
 
 // ------------------------------------------------------------------ host side

@@ -50,12 +50,13 @@ for _ in range(10):
     torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1) * 1e3)
 print(f"B={B}: head {np.median(ts):.1f} us (min {min(ts):.1f})")
-trace = torch.zeros(1024 * 16, dtype=torch.int64, device=dev)
-N.check(N.lib().nanospec_debug_set_trace(trace.data_ptr(), 1024), "trace")
+NT = 8192
+trace = torch.zeros(NT * 16, dtype=torch.int64, device=dev)
+N.check(N.lib().nanospec_debug_set_trace(trace.data_ptr(), NT), "trace")
 run()
 torch.cuda.synchronize()
 N.check(N.lib().nanospec_debug_set_trace(None, 0), "trace")
-t = trace.view(1024, 16).cpu().numpy().astype(np.int64)
+t = trace.view(NT, 16).cpu().numpy().astype(np.int64)
 nA = 148
 A = t[:nA]
 t0 = A[A[:, 0] > 0, 0].min()
@@ -67,6 +68,13 @@ for name, e in (("A start", 0), ("A dep", 1), ("A first loads", 2), ("A last MMA
         r_ = (c - t0) / 1e3
         print(f"    {name:20s} n={len(c):3d} min {r_.min():8.2f} med {np.median(r_):8.2f} max {r_.max():8.2f}")
 print("    tail item 0 cycles: kth", np.median(A[:, 10]), "compact", np.median(A[:, 11]), "cnt", np.median(A[:, 12]), "ranked", np.median(A[:, 13]))
+Bm = t[nA:][t[nA:, 12] == 0xB]
+for name, e in (("M start", 0), ("M dep", 1), ("M heads", 5), ("M cands", 7), ("M done", 4)):
+    c = Bm[:, e]
+    c = c[c > 0]
+    if len(c):
+        r_ = (c - t0) / 1e3
+        print(f"    {name:20s} n={len(c):4d} min {r_.min():8.2f} med {np.median(r_):8.2f} max {r_.max():8.2f}")
 busy = A[:, 8] / 1e3
 units = A[:, 10] + 1
 print(f"    epilogue busy per unit (us): med {np.median(busy / np.maximum(units, 1)):.2f} max {np.max(busy / np.maximum(units, 1)):.2f}; units per CTA {np.bincount(units)}")
