@@ -1151,7 +1151,7 @@ __global__ void __launch_bounds__(kBThreads, 1) head_select_kernel(const __grid_
 // k-th largest list head bounds every top-k key from below; the entries above
 // it are ranked by counting) and folds the lse.
 __global__ void __launch_bounds__(kBThreads, 1) head_select_tiles_kernel(const __grid_constant__ SplitArgs a) {
-  __shared__ uint2 lst[kBWarps][kMaxK];
+  __shared__ uint2 lst[kBWarps][kMaxK + 1];  // +1: lane t reading list t hits distinct banks
   __shared__ float2 sst[kBWarps];
   __shared__ uint2 csw[kBWarps][kBM];  // per-warp candidate scratch, then the merge's candidates
   uint2* cm = &csw[0][0];              // (free once every warp has its list)
@@ -1232,6 +1232,8 @@ __global__ void __launch_bounds__(kBThreads, 1) head_select_tiles_kernel(const _
   }
   if (warp != 0) return;
   // ---- merge the tiles' lists (lane t: tile t)
+  const long long ck0 = clock64();
+  unsigned long long* tr = p.trace ? p.trace + (long long)(a.trace_base + blockIdx.x) * kTraceSlots : nullptr;
   const uint32_t head = has ? lst[lane][0].x : 0u;
   uint32_t v = head;
 #pragma unroll
@@ -1243,6 +1245,7 @@ __global__ void __launch_bounds__(kBThreads, 1) head_select_tiles_kernel(const _
       v = keep_min ? (o < v ? o : v) : (o > v ? o : v);
     }
   const uint32_t T = __shfl_sync(0xffffffffu, v, 32 - k);  // k distinct heads reach it (0: fewer than k tiles)
+  if (tr && lane == 0) tr[8] = clock64() - ck0;
   int c = 0;  // the list is sorted: the entries >= T are a prefix
   if (has) {
 #pragma unroll 8
@@ -1260,6 +1263,7 @@ __global__ void __launch_bounds__(kBThreads, 1) head_select_tiles_kernel(const _
   const int cnt = __shfl_sync(0xffffffffu, pre, 31);
   for (int q = 0; q < c; ++q) cm[pre - c + q] = lst[lane][q];
   __syncwarp();
+  if (tr && lane == 0) { tr[10] = clock64() - ck0; tr[11] = cnt; }
   const long long ob = ((long long)seq * p.n + node) * k;
   for (int q = lane; q < cnt; q += 32) {
     const uint2 me = cm[q];
@@ -1278,6 +1282,7 @@ __global__ void __launch_bounds__(kBThreads, 1) head_select_tiles_kernel(const _
     a.topk_logit[ob + q] = -INFINITY;
     a.topk_id[ob + q] = -1;
   }
+  if (tr && lane == 0) tr[13] = clock64() - ck0;
   if (tid == 0) trace_b(a, 4);
 }
 

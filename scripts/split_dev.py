@@ -126,6 +126,10 @@ if args.trace:
                 cyc = rows_[ok, 15] - rows_[ok, 14]
                 ns = rows_[ok, 9 if nm == "A" else 4] - rows_[ok, 0 if nm == "A" else 1]
                 print(f"    {nm} SM clock ~{np.median(cyc / np.maximum(ns, 1)) * 1e3:.0f} MHz")
+        Bt = t[nA:nA + 512][t[nA:nA + 512, 12] == 0xB]
+        if len(Bt):
+            print("    B merge cycles: threshold", np.median(Bt[:, 8]), "staged", np.median(Bt[:, 10]),
+                  "cands", np.median(Bt[:, 11]), "ranked+stored", np.median(Bt[:, 13]))
         for name, e in (("B start", 0), ("B dep", 1), ("B loaded", 5), ("B hist1", 6), ("B S1", 2), ("B cands", 7), ("B ranked", 9), ("B tiles", 3), ("B done", 4)):
             c = t[nA:nA + 512, e]
             c = c[c > 0]
