@@ -89,75 +89,7 @@ __device__ __forceinline__ uint32_t ld_acquire(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
-  unsigned old;
-  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
-}
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ uint4 ld_relaxed_v4(const void* p) {
-  uint4 v;
-  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ uint2 ld_relaxed_v2(const void* p) {
-  uint2 v;
-  asm volatile("ld.relaxed.gpu.global.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed_f32(float* p, float v) {
-  asm volatile("st.relaxed.gpu.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
-}
-__device__ __forceinline__ void st_relaxed_v2(uint2* p, uint2 v) {
-  asm volatile("st.relaxed.gpu.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
-}
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// Address of the same shared-memory location in CTA `rank` of the cluster.
-__device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ float4 ld_dsmem_v4(uint32_t caddr) {
-  float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(caddr)
-               : "memory");
-  return v;
-}
-__device__ __forceinline__ uint32_t ld_dsmem_u32(uint32_t caddr) {
-  uint32_t v;
-  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(caddr) : "memory");
-  return v;
-}
-__device__ __forceinline__ uint2 ld_dsmem_u2(uint32_t caddr) {
-  uint2 v;
-  asm volatile("ld.shared::cluster.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(caddr) : "memory");
-  return v;
-}
-__device__ __forceinline__ float2 ld_dsmem_f2(uint32_t caddr) {
-  float2 v;
-  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(caddr) : "memory");
-  return v;
-}
-__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v);
-__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 __device__ __forceinline__ void red_add_release(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -172,13 +104,6 @@ __device__ __forceinline__ float key_value(uint32_t kk) {
 // (value desc, id asc): a before b
 __device__ __forceinline__ bool key_before(uint32_t ka, uint32_t ga, uint32_t kb, uint32_t gb) {
   return ka > kb || (ka == kb && ga < gb);
-}
-// Compare-exchange: afterwards entry a precedes entry b in (value desc, id asc).
-__device__ __forceinline__ void cx(uint32_t& ka, uint32_t& ga, uint32_t& kb, uint32_t& gb) {
-  if (key_before(kb, gb, ka, ga)) {
-    const uint32_t tk = ka; ka = kb; kb = tk;
-    const uint32_t tg = ga; ga = gb; gb = tg;
-  }
 }
 // Online lse partial: fold (m2, e2) into (m, e), e = sum exp(z - m).
 __device__ __forceinline__ void lse_fold(float& m, float& e, float m2, float e2) {
@@ -198,26 +123,6 @@ __device__ __forceinline__ uint32_t warp_kth_key(uint32_t x, int k) {
   }
   const unsigned sel = __ballot_sync(0xffffffffu, rank == k - 1);
   return __shfl_sync(0xffffffffu, x, __ffs(sel) - 1);
-}
-// Rank `cnt` staged (key, gid) candidates by counting (all loads independent)
-// and write the k best, best first, to out[0..k).
-__device__ __forceinline__ void warp_rank_write(const uint2* cs, int cnt, int k, uint2* out) {
-  const int lane = threadIdx.x & 31;
-  for (int e = lane; e < cnt; e += 32) {
-    const uint2 me = cs[e];
-    int r = 0;
-    for (int f = 0; f < cnt; ++f) {
-      const uint2 o = cs[f];
-      r += key_before(o.x, o.y, me.x, me.y) ? 1 : 0;
-    }
-    if (r < k) out[r] = me;
-  }
-}
-// Threshold selection of a warp's top-k from 4 entries per lane (unsorted):
-// T = k-th largest lane maximum (k lanes each own an entry >= T, so every
-// top-k entry is >= T); the entries >= T are compacted into `scratch` and
-__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
 }
 
 }  // namespace
