@@ -1433,7 +1433,8 @@ int g_stream_only = 0;  // debug mode 1: kernel A alone (measurement; no outputs
 // experiments (NANOSPEC_SPLIT_FLAGS): 1 = skip kernel B, 2 = no PDL, 16 = kernel B alone,
 // 32 = one K atom per pipeline stage, 64 = no 256-row units in the persistent mode,
 // 128 = one K atom per stage with 256-row units, 256 = no list mode (split-K 1: partial tiles + select kernel),
-// 512 = the radix select kernel for one-round heads (instead of per-tile warp lists)
+// 512 = the radix select kernel for one-round heads (instead of per-tile warp lists),
+// 8192 = list mode of one sequence with 2 K atoms per stage (and tile pairs when tiles >= 2 x SMs)
 int g_split_flags = -1;
 int split_flags() {
   if (g_split_flags < 0) {
@@ -1590,6 +1591,11 @@ cudaError_t launch_list_pair(const SplitArgs& a, int grid_a, cudaStream_t stream
 
 cudaError_t launch_list(const SplitArgs& a, int grid_a, cudaStream_t stream) {
   const int n = a.p.n;
+  if (a.ut == 1 && a.p.batch == 1 && !(split_flags() & 8192)) {  // one sequence: 512 / 384 contiguous bytes of a row per stage
+    if (n <= 16) return launch_list_pair<16, 4, 1>(a, grid_a, stream);
+    if (n <= 32) return launch_list_pair<32, 4, 1>(a, grid_a, stream);
+    if (n <= 64) return launch_list_pair<64, 3, 1>(a, grid_a, stream);
+  }
   if (a.ut == 2) {
     if (n <= 16) return launch_list_pair<16, 2, 2>(a, grid_a, stream);
     if (n <= 32) return launch_list_pair<32, 2, 2>(a, grid_a, stream);
@@ -1677,6 +1683,13 @@ cudaError_t launch_head_tc(const HeadProblem& p, int k, float* topk_logit, int32
     a.ut = 2;
     a.upt = (a.tps + 1) / 2;
     a.units = p.batch * a.upt;
+  }
+  if (a.ut == 2 && p.batch == 1 && p.n <= 64 && !(split_flags() & 8192)) {
+    // one sequence (the dense [0, V) head, verify top-k): single-tile units with
+    // 3-4 K atoms per stage stream better than tile pairs with 2 (measured:
+    // verify top-3 x 6 positions 208 -> 202 us); batched heads keep the pairs
+    a.ut = 1;
+    a.units = a.ntiles;
   }
   a.heads = a.units < G ? a.units : G;
   // more tiles than SMs (split-K 1, persistent): the tiles are reduced to

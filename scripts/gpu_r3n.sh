@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+for f in 0 8192 0 8192; do
+  echo "flags $f"
+  NANOSPEC_SPLIT_FLAGS=$f timeout 600 python bench.py --config dp64 --steps 20 --warmup 3 2>&1 | tail -1 | python -c "import json,sys; j=json.loads(sys.stdin.read()); print(j['value'], j['breakdown'])"
+  NANOSPEC_SPLIT_FLAGS=$f timeout 900 python bench.py --steps 30 --warmup 5 --no-cpu --replays 3 2>&1 | tail -1 | python -c "import json,sys; j=json.loads(sys.stdin.read()); print(j['value'], j['dense'])"
+done
