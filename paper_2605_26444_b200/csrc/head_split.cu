@@ -120,6 +120,7 @@ struct SplitArgs {
   int32_t* topk_id;
   float* lse;           // [batch][n] or null
   int k;
+  int plain;            // 1: the stream kernel waits for the previous grid at its start (experiment flag 16384)
   long long list_stats; // list mode: byte offset (in part) of the [tiles][n] (M, sum exp) lse partials
   long long dbg_ld;     // debug logits: floats between the rows of one (sequence, node)
   int trace_base;       // debug trace: B's CTA b writes trace row trace_base + b (after A's rows)
@@ -530,9 +531,18 @@ __global__ void __launch_bounds__(LIST ? kAThreadsL : kAThreads, 1) head_stream_
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p.ids_base + (long long)cur.seq * p.ids_stride + cur.tile * kBM + 32 * tid));
     if (tid == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.nact_base + (long long)cur.seq * p.nact_stride));
   }
-  // everything above overlaps the previous kernel; its results (the state)
-  // are read only after this
-  pdl_wait();
+  // The previous kernel on the stream is either not programmatic (this grid
+  // then starts after it completed) or one of this library's select / merge
+  // kernels, which trigger only after their own wait, i.e. once the stream
+  // kernel before them -- the last writer of the state this grid reads -- has
+  // completed (the state update kernel does not trigger early).  So the row
+  // ids, the lists and the hidden states may be read right away; only the
+  // scratch (row-id table, partial tiles, drop words), which that select
+  // kernel may still be reading, waits for it: the streaming CTAs wait just
+  // before their drain, the updater before it starts.  The stream of step
+  // s + 1 overlaps the select kernel of step s.  (List mode keeps the plain
+  // order: its epilogue writes from the first unit on.)
+  if (LIST || a.plain) pdl_wait();
   // B (which waits for this grid to complete) may be scheduled now
   asm volatile("griddepcontrol.launch_dependents;");
   tc_fence_before();
@@ -554,6 +564,7 @@ __global__ void __launch_bounds__(LIST ? kAThreadsL : kAThreads, 1) head_stream_
     UpdSmem& us = *reinterpret_cast<UpdSmem*>(base);
     uint32_t* words = reinterpret_cast<uint32_t*>(base + (sizeof(UpdSmem) + 255) / 256 * 256);
     SplitPublish pub{&a, words};
+    pdl_wait();  // the previous select kernel has read the drop words; the state is then final
     update_fast(a.upd, a.upd.seq0, us, pub, p.trace);
     if (tid == 0) trace_mark(p.trace, 11);
   } else {
@@ -598,12 +609,6 @@ __global__ void __launch_bounds__(LIST ? kAThreadsL : kAThreads, 1) head_stream_
         red_add_release(a.arrive_ctr, 1u);
         arrived = true;
       }
-      // the tile's row ids for B (split 0 only); rows past the list: -1
-      if (un.split == 0 && un.tile == 0 && tid == kRows) a.mrows[un.seq] = sh_m[buf];
-      if (un.split == 0 && tid < kRows && (un.tile >= a.tps || un.tile * kBM + tid < a.tps * kBM)) {
-        const int32_t g = tid < rows ? ids_s[buf][tid] : -1;
-        a.rowgid[((long long)un.seq * (a.tps + a.n_patch) + un.tile) * kBM + tid] = g;
-      }
       const int un_next = u + stride;
       int32_t nx_id = -1;
       int nx_m = 0;
@@ -618,6 +623,12 @@ __global__ void __launch_bounds__(LIST ? kAThreadsL : kAThreads, 1) head_stream_
         }
       }
       if (rows <= 0) {
+        if (!LIST) {  // no rows: the row-id table still says so (after the previous select kernel)
+          pdl_wait();
+          if (un.split == 0 && un.tile == 0 && tid == kRows) a.mrows[un.seq] = sh_m[buf];
+          if (un.split == 0 && tid < kRows && (un.tile >= a.tps || un.tile * kBM + tid < a.tps * kBM))
+            a.rowgid[((long long)un.seq * (a.tps + a.n_patch) + un.tile) * kBM + tid] = -1;
+        }
         if (nx) {
           if (tid < kRows) ids_s[buf ^ 1][tid] = nx_id;
           if (tid == kRows) sh_m[buf ^ 1] = nx_m;
@@ -684,7 +695,19 @@ __global__ void __launch_bounds__(LIST ? kAThreadsL : kAThreads, 1) head_stream_
           }
         }
         if (tid == 0 && local == 0) trace_mark(p.trace, 3);
-        if (!LIST) {
+        if (LIST) {
+          // the tile's row ids (split 0 only; rows past the list: -1) -- list mode waited at the start
+          if (un.split == 0 && un.tile == 0 && tid == kRows) a.mrows[un.seq] = sh_m[buf];
+          if (un.split == 0 && tid < kRows && (un.tile >= a.tps || un.tile * kBM + tid < a.tps * kBM))
+            a.rowgid[((long long)un.seq * (a.tps + a.n_patch) + un.tile) * kBM + tid] = tid < rows ? ids_s[buf][tid] : -1;
+        } else {
+        // ---------------- the scratch: the previous select kernel has completed
+        if (nrun == 0) pdl_wait();
+        // the tile's row ids for B (split 0 only); rows past the list: -1
+        if (un.split == 0 && un.tile == 0 && tid == kRows) a.mrows[un.seq] = sh_m[buf];
+        if (un.split == 0 && tid < kRows && (un.tile >= a.tps || un.tile * kBM + tid < a.tps * kBM))
+          a.rowgid[((long long)un.seq * (a.tps + a.n_patch) + un.tile) * kBM + tid] = tid < rows ? ids_s[buf][tid] : -1;
+        if (tid == 0 && nrun == 0) trace_mark(p.trace, 1);
         // ---------------- drain: TMEM -> the unit's partial tile in L2
         mbar_wait(smem_u32(&bars[2 * C::kStages]), nrun & 1);
         tc_fence_after();
@@ -1434,7 +1457,8 @@ int g_stream_only = 0;  // debug mode 1: kernel A alone (measurement; no outputs
 // 32 = one K atom per pipeline stage, 64 = no 256-row units in the persistent mode,
 // 128 = one K atom per stage with 256-row units, 256 = no list mode (split-K 1: partial tiles + select kernel),
 // 512 = the radix select kernel for one-round heads (instead of per-tile warp lists),
-// 8192 = list mode of one sequence with 2 K atoms per stage (and tile pairs when tiles >= 2 x SMs)
+// 8192 = list mode of one sequence with 2 K atoms per stage (and tile pairs when tiles >= 2 x SMs),
+// 16384 = the stream kernel waits for the previous grid at its start (no overlap with the previous select)
 int g_split_flags = -1;
 int split_flags() {
   if (g_split_flags < 0) {
@@ -1634,6 +1658,7 @@ SplitArgs base_args(const HeadProblem& p, int k, float* topk_logit, int32_t* top
   a.k = k;
   a.tps = (p.max_ids + kBM - 1) / kBM;
   a.dbg_ld = p.max_ids;
+  a.plain = (split_flags() & 16384) ? 1 : 0;
   return a;
 }
 

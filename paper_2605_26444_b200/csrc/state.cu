@@ -207,8 +207,9 @@ __global__ void __launch_bounds__(kFastThreads) state_update_fast_kernel(AppendA
   // not touch the state before that kernel has completed.
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (threadIdx.x == 0) trace_mark(trace, 9);  // state: start
-  // let the dependent head kernel get resident and run its prologue meanwhile
-  asm volatile("griddepcontrol.launch_dependents;");
+  // no early griddepcontrol.launch_dependents: the head's stream kernel reads
+  // the state before its own grid-dependency wait, so it may start only when
+  // this update is complete
   NoPublish hook;
   update_fast(args, args.seq0 + blockIdx.x, sm, hook, trace);
 }
