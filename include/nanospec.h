@@ -23,7 +23,16 @@
  *   - Asynchrony: every call except nanospec_state_read / nanospec_state_check
  *     is asynchronous on `stream`, never synchronises the host and never copies
  *     the active-set size to the host.  Update -> head ordering is
- *     stream order.
+ *     stream order.  The tensor-core head kernels are launched with
+ *     programmatic dependent launch and read their INPUTS (state, hidden
+ *     states, update lists) as soon as the previous kernel on the stream lets
+ *     them start; they wait for that kernel to complete only before writing
+ *     the head scratch.  This library's own kernels never let a dependent
+ *     start before their outputs that such an input could come from are
+ *     complete; a caller mixing in its own programmatic-launch kernels that
+ *     produce these inputs must not trigger (griddepcontrol.launch_dependents)
+ *     before those outputs are written.  Ordinary kernels, copies and event
+ *     waits need nothing.
  *   - Errors: host-side validation -> NANOSPEC_EINVAL (nothing launched);
  *     launch failure -> NANOSPEC_ECUDA.  An out-of-range token id cannot be
  *     checked on the host: the kernels drop it (it is never appended) and set a
