@@ -52,6 +52,10 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <mutex>
+#include <utility>
+#include <vector>
+
 #include "common.cuh"
 #include "internal.h"
 #include "state_fast.cuh"
@@ -1666,7 +1670,31 @@ bool shape_ok(const HeadProblem& p, int k) {
   return p.d % kBK == 0 && p.n >= 1 && p.n <= 256 && p.ldw % 8 == 0 && k >= 1 && k <= kMaxK && p.d / kBK >= 1;
 }
 
+std::mutex g_upd_mu;
+std::vector<std::pair<int, cudaStream_t>> g_upd_streams;  // (device, stream) whose last launch was an update
+
 }  // namespace
+
+void note_update_launch(cudaStream_t stream) {
+  int dev = 0;
+  (void)cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_upd_mu);
+  for (auto& e : g_upd_streams)
+    if (e.first == dev && e.second == stream) return;
+  g_upd_streams.emplace_back(dev, stream);
+}
+
+bool take_update_launch(cudaStream_t stream) {
+  int dev = 0;
+  (void)cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_upd_mu);
+  for (size_t i = 0; i < g_upd_streams.size(); ++i)
+    if (g_upd_streams[i].first == dev && g_upd_streams[i].second == stream) {
+      g_upd_streams.erase(g_upd_streams.begin() + (long)i);
+      return true;
+    }
+  return false;
+}
 
 size_t head_tc_scratch_bytes(int batch, int max_ids, int n) { return split_layout(batch, max_ids, n, 256).total; }
 
@@ -1697,6 +1725,7 @@ cudaError_t launch_head_tc(const HeadProblem& p, int k, float* topk_logit, int32
   const SplitLayout L = split_layout(p.batch, p.max_ids, p.n, 256);
   if (L.total > scratch_bytes) return cudaErrorInvalidValue;
   SplitArgs a = base_args(p, k, topk_logit, topk_id, lse, scratch, L);
+  if (take_update_launch(stream)) a.plain = 1;  // right after an update kernel: wait before reading the state
   a.n_patch = 0;
   a.ntiles = p.batch * a.tps;
   plan_splits(a, G, p.d / kBK);
@@ -1744,6 +1773,7 @@ cudaError_t launch_step_tc(const HeadProblem& p, const AppendArgs& upd, int k, f
   const SplitLayout L = split_layout(1, p.max_ids, p.n, 256);
   if (L.total > scratch_bytes) return cudaErrorInvalidValue;
   SplitArgs a = base_args(p, k, topk_logit, topk_id, lse, scratch, L);
+  if (take_update_launch(stream)) a.plain = 1;
   a.n_patch = n_patch;
   a.ntiles = tps + n_patch;
   plan_splits(a, G - 1, p.d / kBK);

@@ -63,6 +63,12 @@ struct AppendArgs;
 cudaError_t launch_step_tc(const HeadProblem& p, const AppendArgs& upd, int k, float* topk_logit, int32_t* topk_id,
                            float* lse, void* scratch, size_t scratch_bytes, int num_sms, cudaStream_t stream,
                            bool dry_run = false);
+// The state update kernel lets its dependent start early; a tensor-core head
+// launched right after it on the same stream must then wait for it before
+// reading the state.  note_update_launch records (device, stream);
+// take_update_launch reports and clears it (head_split.cu).
+void note_update_launch(cudaStream_t stream);
+bool take_update_launch(cudaStream_t stream);
 // Whether launch_state_append would take the per-step fast path for these lists.
 bool state_fast_path(const StateView& sv, int reset, long long a_len, int a_dedup, long long b_len, int b_dedup);
 // Debug: -1 default; 0 = launch the head's kernels without programmatic

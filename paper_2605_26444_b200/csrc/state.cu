@@ -207,9 +207,10 @@ __global__ void __launch_bounds__(kFastThreads) state_update_fast_kernel(AppendA
   // not touch the state before that kernel has completed.
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (threadIdx.x == 0) trace_mark(trace, 9);  // state: start
-  // no early griddepcontrol.launch_dependents: the head's stream kernel reads
-  // the state before its own grid-dependency wait, so it may start only when
-  // this update is complete
+  // let the dependent head kernel get resident and run its prologue meanwhile
+  // (the launcher records this stream, so that head waits for this grid before
+  // reading the state: note_update_launch)
+  asm volatile("griddepcontrol.launch_dependents;");
   NoPublish hook;
   update_fast(args, args.seq0 + blockIdx.x, sm, hook, trace);
 }
@@ -247,6 +248,7 @@ cudaError_t launch_state_append(const StateView& sv, int seq0, int nseq, int res
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     unsigned long long* tr = trace_buffer();
+    note_update_launch(stream);
     cudaError_t e = cudaLaunchKernelEx(&cfg, state_update_fast_kernel, args, tr);
     if (e != cudaSuccess) {
       (void)cudaGetLastError();
