@@ -27,9 +27,11 @@
  *     programmatic dependent launch and read their INPUTS (state, hidden
  *     states, update lists) as soon as the previous kernel on the stream lets
  *     them start; they wait for that kernel to complete only before writing
- *     the head scratch.  This library's own kernels never let a dependent
- *     start before their outputs that such an input could come from are
- *     complete; a caller mixing in its own programmatic-launch kernels that
+ *     the head scratch.  This library's select kernels let a dependent start
+ *     only after the state's last writer completed; its state update kernel
+ *     lets the next kernel start early, and the library then makes the next
+ *     tensor-core head launched on that stream wait before reading the state.
+ *     A caller mixing in its own programmatic-launch kernels that
  *     produce these inputs must not trigger (griddepcontrol.launch_dependents)
  *     before those outputs are written.  Ordinary kernels, copies and event
  *     waits need nothing.
